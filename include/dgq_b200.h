@@ -1,0 +1,155 @@
+/*
+ * dgq_b200.h — C ABI of the B200-native DGQ A8W4 linear-layer hot path.
+ *
+ * Plain pointers, sizes and status codes only (no CUDA, torch or C++ types),
+ * so a cgo / JNI / ctypes binding is a direct transcription.  Device pointers
+ * are prefixed d; `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Every function returns dgq_status; on failure
+ * dgq_last_error() holds a thread-local message and dgq_last_error_field() the
+ * offending DgqLayer field for DGQ_EVALIDATION (mirrors dgq::validation_error).
+ *
+ * The C++ operator API of the reference (proj/include/dgq/kernel.hpp,
+ * proj/include/dgq/format.hpp) is implemented on top of these entry points by
+ * paper_2310_04836_b200/csrc/dropin.cpp (include/dgq/*.hpp).  Status codes map
+ * back to the reference's exception taxonomy:
+ *   DGQ_EINVAL      -> std::invalid_argument   (proj/src/kernel.cpp:15-19,47-54,92-98)
+ *   DGQ_EVALIDATION -> dgq::validation_error   (proj/src/format.cpp:18-20,131-136)
+ *   DGQ_EOVERFLOW   -> std::runtime_error      (proj/src/kernel.cpp:83-85)
+ *   DGQ_EFORMAT     -> dgq::format_error       (proj/src/format.cpp:214-250)
+ */
+#ifndef DGQ_B200_H
+#define DGQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGQ_B200_ABI_VERSION 1
+
+typedef enum dgq_status {
+  DGQ_OK = 0,
+  DGQ_EINVAL = 1,
+  DGQ_EVALIDATION = 2,
+  DGQ_EOVERFLOW = 3,
+  DGQ_ECUDA = 4,
+  DGQ_ENOMEM = 5,
+  DGQ_EFORMAT = 6
+} dgq_status;
+
+enum { DGQ_MODE_STATIC = 0, DGQ_MODE_DYNAMIC = 1 };      /* proj/include/dgq/format.hpp:32 ActMode */
+enum { DGQ_OUT_F32 = 0, DGQ_OUT_F16 = 1 };
+
+/* Opaque device-resident prepared layer: the DgqLayer of
+ * proj/include/dgq/format.hpp:36-49, validated on the host, uploaded once and
+ * repacked into the B200 tile layout (optionally one column shard of it).
+ * Immutable after creation; safe to share across host threads and streams
+ * (split-K workspaces are per call, see dgq_linear). */
+typedef struct dgq_layer dgq_layer;
+
+typedef struct dgq_layer_info {
+  size_t h;          /* input channels (K) */
+  size_t o_full;     /* output channels of the unsharded layer */
+  size_t o;          /* output channels held by this shard */
+  size_t col_begin;  /* first output channel of this shard */
+  size_t g;          /* group size */
+  size_t k_pad;      /* activation-code row stride the GEMM expects (h rounded up to 128) */
+  size_t n_pad;      /* o rounded up to 128 */
+  int mode;          /* DGQ_MODE_* */
+  float act_scale;
+  int fused;         /* 1: INT4 tiles + in-kernel dequant; 0: materialised INT8 (exotic g) */
+  size_t device_bytes;
+} dgq_layer_info;
+
+int dgq_abi_version(void);
+const char* dgq_last_error(void);
+const char* dgq_last_error_field(void);
+
+/* ---- host-side numerics / invariants (no GPU) ------------------------------ */
+/* replaces dgq::validate_layer, proj/src/format.cpp:24-75 (host arrays, reference layout) */
+dgq_status dgq_validate_layer(size_t h, size_t o, size_t g, int mode, float act_scale, const uint8_t* codes_u4,
+                              const int8_t* s2, const uint8_t* zp_u4, const float* s1, const float* k);
+/* replaces dgq::clip_interval, proj/src/search.cpp:190-201 */
+dgq_status dgq_clip_interval(int s2, int zp, int* lo, int* hi);
+/* replaces dgq::fp16_round, proj/src/quant.cpp:9-58 */
+float dgq_fp16_round(float x);
+
+/* ---- prepared layer ---------------------------------------------------------
+ * Host arrays in the reference layout (codes u4 [h x o] packed along o, even
+ * column in the low nibble; s2 int8 [h/g x o]; zp u4 [h/g x o]; s1 f32[o];
+ * k f32[h]).  Output channels [col_begin, col_end) are kept (col_end == 0
+ * means o): the column-parallel shard of SURVEY.md §8e.  validate != 0 runs
+ * the reference invariants first (DGQ_EVALIDATION + field on failure). */
+dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, float act_scale,
+                            const uint8_t* codes_u4, const int8_t* s2, const uint8_t* zp_u4, const float* s1,
+                            const float* k, size_t col_begin, size_t col_end, int validate, void* stream,
+                            dgq_layer** out);
+/* DGQ1 artifact bytes (proj/include/dgq/format.hpp:6-21, dgq_from_bytes
+ * proj/src/format.cpp:214-266) straight to a prepared (sharded) layer. */
+dgq_status dgq_layer_create_from_dgq1(int device, const uint8_t* bytes, size_t nbytes, size_t col_begin,
+                                      size_t col_end, void* stream, dgq_layer** out);
+void dgq_layer_destroy(dgq_layer* layer);
+dgq_status dgq_layer_get_info(const dgq_layer* layer, dgq_layer_info* info);
+
+/* Bytes of zero-initialised scratch dgq_linear may need for M tokens (split-K
+ * partial sums + tile counters; 0 when the call does not split K).  The
+ * workspace is left zeroed on return, so it can be reused call after call. */
+size_t dgq_linear_workspace_bytes(const dgq_layer* layer, size_t M);
+
+/* ---- K1: per-token INT8 activation quantisation ----------------------------
+ * replaces dgq::quantize_activations, proj/src/kernel.cpp:14-44.
+ * dXq rows use stride ldq >= h (pass info.k_pad for dgq_linear); pad columns
+ * are zero-filled. */
+dgq_status dgq_quantize_act(const dgq_layer* layer, const float* dX, size_t M, size_t ldx, int8_t* dXq, size_t ldq,
+                            float* dRowScale, void* stream);
+dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx, const float* dK, int mode,
+                                float act_scale, int8_t* dXq, size_t ldq, float* dRowScale, void* stream);
+
+/* ---- K5: fused DGQ linear (INT4 dequant prologue + tcgen05 kind::i8 + epilogue)
+ * replaces int8_gemm + epilogue of dgq::dgq_forward, proj/src/kernel.cpp:144-153.
+ * dXq: [M x ldq] codes from K1 (ldq must equal info.k_pad, 16-B aligned).
+ * dY:  [M x ldy] f32 or f16 (out_dtype); fp16_mode selects the reference's
+ *      binary16 epilogue (proj/src/kernel.cpp:105-108).  dY may be NULL.
+ * dAcc: optional raw int32 accumulators [M x ld_acc].
+ * dWorkspace: dgq_linear_workspace_bytes(layer, M) zeroed bytes, or NULL to use
+ *      the layer's internal workspace (then calls on the same layer must be
+ *      stream-ordered). */
+dgq_status dgq_linear(const dgq_layer* layer, const int8_t* dXq, size_t ldq, const float* dRowScale, size_t M,
+                      const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
+                      size_t ld_acc, void* dWorkspace, size_t ws_bytes, void* stream);
+/* K1 + K5 in one call; dXq [M x k_pad] and dRowScale [M] are caller scratch. */
+dgq_status dgq_forward_device(const dgq_layer* layer, const float* dX, size_t M, size_t ldx, const float* dBias,
+                              int out_dtype, void* dY, size_t ldy, int8_t* dXq, float* dRowScale, void* dWorkspace,
+                              size_t ws_bytes, void* stream);
+
+/* ---- K2s: INT4 -> INT8 dequantisation ---------------------------------------
+ * replaces dgq::dequantize_to_s8, proj/src/format.cpp:122-141.
+ * From a prepared layer (same dequantiser as K5) into dW [h x ldw]: */
+dgq_status dgq_layer_dequant_s8(const dgq_layer* layer, int8_t* dW, size_t ldw, void* stream);
+/* From reference-layout device arrays, with the reference's range check
+ * (synchronises the stream; DGQ_EVALIDATION field "codes" on corruption): */
+dgq_status dgq_dequantize_to_s8(size_t h, size_t o, size_t g, const uint8_t* d_codes_u4, const int8_t* d_s2,
+                                const uint8_t* d_zp_u4, int8_t* dW, void* stream);
+
+/* ---- K3: exact INT8 GEMM (tcgen05 kind::i8) ---------------------------------
+ * replaces dgq::int8_gemm, proj/src/kernel.cpp:46-87.  dXq [M x ldx], dW [K x ldw]
+ * row-major, dAcc [M x ld_acc] int32.  max_abs_acc (HOST pointer, may be NULL)
+ * runs the running-sum audit and synchronises the stream. */
+dgq_status dgq_int8_gemm(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K, size_t N,
+                         int32_t* dAcc, size_t ld_acc, int64_t* max_abs_acc, void* stream);
+
+/* ---- K4: standalone epilogue -------------------------------------------------
+ * replaces dgq::epilogue, proj/src/kernel.cpp:89-116. */
+dgq_status dgq_epilogue(const int32_t* dAcc, size_t lda, const float* dRowScale, const float* dS1, const float* dBias,
+                        size_t M, size_t N, int fp16_mode, int out_dtype, void* dY, size_t ldy, void* stream);
+
+/* ---- audit: max over (r,c,i) of |running sum| (proj/src/kernel.cpp:73-77) --- */
+dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K,
+                                 size_t N, int64_t* max_abs_acc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGQ_B200_H */

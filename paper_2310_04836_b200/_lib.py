@@ -1,0 +1,125 @@
+"""ctypes binding of libdgq_b200.so (the C ABI in include/dgq_b200.h).
+
+The library is the only compute path: if it is missing or fails to load this
+module raises — there is no CPU or PyTorch fallback."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdgq_b200.so")
+
+_vp, _sz, _i, _f = C.c_void_p, C.c_size_t, C.c_int, C.c_float
+
+DGQ_OK, DGQ_EINVAL, DGQ_EVALIDATION, DGQ_EOVERFLOW, DGQ_ECUDA, DGQ_ENOMEM, DGQ_EFORMAT = range(7)
+MODE_STATIC, MODE_DYNAMIC = 0, 1
+OUT_F32, OUT_F16 = 0, 1
+
+
+class DgqError(RuntimeError):
+    """Base class; `status` is the dgq_status code."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+class ValidationError(DgqError, ValueError):
+    """dgq::validation_error (proj/include/dgq/error.hpp): names the field."""
+
+    def __init__(self, status, msg, field):
+        super().__init__(status, msg)
+        self.field = field
+
+
+class FormatError(DgqError, ValueError):
+    """dgq::format_error: `kind` in {bad_magic, truncated, size_mismatch, unknown_dtype, bad_header}."""
+
+    def __init__(self, status, msg, kind):
+        super().__init__(status, msg)
+        self.kind = kind
+
+
+class InvalidArgument(DgqError, ValueError):
+    """std::invalid_argument."""
+
+
+class OverflowRuntimeError(DgqError):
+    """std::runtime_error (accumulator overflow)."""
+
+
+class LayerInfo(C.Structure):
+    _fields_ = [("h", _sz), ("o_full", _sz), ("o", _sz), ("col_begin", _sz), ("g", _sz), ("k_pad", _sz),
+                ("n_pad", _sz), ("mode", _i), ("act_scale", _f), ("fused", _i), ("device_bytes", _sz)]
+
+
+_SIGS = {
+    "dgq_abi_version": (_i, []),
+    "dgq_last_error": (C.c_char_p, []),
+    "dgq_last_error_field": (C.c_char_p, []),
+    "dgq_validate_layer": (_i, [_sz, _sz, _sz, _i, _f, _vp, _vp, _vp, _vp, _vp]),
+    "dgq_clip_interval": (_i, [_i, _i, C.POINTER(_i), C.POINTER(_i)]),
+    "dgq_fp16_round": (_f, [_f]),
+    "dgq_layer_create": (_i, [_i, _sz, _sz, _sz, _i, _f, _vp, _vp, _vp, _vp, _vp, _sz, _sz, _i, _vp,
+                              C.POINTER(_vp)]),
+    "dgq_layer_create_from_dgq1": (_i, [_i, _vp, _sz, _sz, _sz, _vp, C.POINTER(_vp)]),
+    "dgq_layer_destroy": (None, [_vp]),
+    "dgq_layer_get_info": (_i, [_vp, C.POINTER(LayerInfo)]),
+    "dgq_linear_workspace_bytes": (_sz, [_vp, _sz]),
+    "dgq_quantize_act": (_i, [_vp, _vp, _sz, _sz, _vp, _sz, _vp, _vp]),
+    "dgq_quantize_act_raw": (_i, [_vp, _sz, _sz, _sz, _vp, _i, _f, _vp, _sz, _vp, _vp]),
+    "dgq_linear": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _i, _vp, _sz, _vp, _sz, _vp, _sz, _vp]),
+    "dgq_forward_device": (_i, [_vp, _vp, _sz, _sz, _vp, _i, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "dgq_layer_dequant_s8": (_i, [_vp, _vp, _sz, _vp]),
+    "dgq_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
+    "dgq_int8_gemm": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, _vp, _sz, C.POINTER(C.c_int64), _vp]),
+    "dgq_epilogue": (_i, [_vp, _sz, _vp, _vp, _vp, _sz, _sz, _i, _i, _vp, _sz, _vp]),
+    "dgq_audit_max_abs_acc": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, C.POINTER(C.c_int64), _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load (once) and return the CDLL; raises if the extension was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2310_04836_b200.build` "
+                                  "(there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def check(status: int):
+    if status == DGQ_OK:
+        return
+    L = lib()
+    msg = (L.dgq_last_error() or b"").decode(errors="replace")
+    field = (L.dgq_last_error_field() or b"").decode(errors="replace")
+    if status == DGQ_EVALIDATION:
+        raise ValidationError(status, msg, field)
+    if status == DGQ_EFORMAT:
+        raise FormatError(status, msg, field)
+    if status == DGQ_EINVAL:
+        raise InvalidArgument(status, msg)
+    if status == DGQ_EOVERFLOW:
+        raise OverflowRuntimeError(status, msg)
+    if status == DGQ_ENOMEM:
+        raise MemoryError(msg)
+    raise DgqError(status, msg)

@@ -1,0 +1,592 @@
+// C-ABI entry points (include/dgq_b200.h): argument checks with the reference's
+// error semantics, prepared-layer lifetime, TMA descriptor construction and
+// kernel dispatch.  No CPU compute path exists: every numeric result comes
+// from a CUDA kernel in this library.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dgq_b200.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string t_msg;
+thread_local std::string t_field;
+
+dgq_status fail(dgq_status st, const std::string& msg, const std::string& field = "") {
+  t_msg = msg;
+  t_field = field;
+  return st;
+}
+
+#define DGQ_CUDA(expr)                                                                           \
+  do {                                                                                           \
+    cudaError_t e_ = (expr);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(e_ == cudaErrorMemoryAllocation ? DGQ_ENOMEM : DGQ_ECUDA,                      \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                           \
+  } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D uint8 tensor map: rows x cols (cols contiguous, row stride `ld` bytes),
+// box = box_rows x 128 bytes, 128-byte swizzle, zero fill out of bounds.
+dgq_status make_tmap(CUtensorMap* m, const void* base, size_t rows, size_t cols, size_t ld, uint32_t box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld)};
+  cuuint32_t box[2] = {128u, box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return DGQ_OK;
+}
+
+size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+inline int nib(const uint8_t* p, size_t idx) { return (idx & 1) ? (p[idx >> 1] >> 4) : (p[idx >> 1] & 0x0F); }
+
+}  // namespace
+
+struct dgq_layer {
+  int device = 0;
+  size_t h = 0, o_full = 0, o = 0, c0 = 0, g = 0;
+  int mode = 1;
+  float act_scale = 0.0f;
+  size_t k_pad = 0, n_pad = 0;
+  int n_tiles = 0, k_blocks = 0;
+  bool fused = true;
+  uint8_t* tiles = nullptr;  // fused: prepared INT4 tiles
+  int8_t* wt = nullptr;      // non-fused: W_s8^T [n_pad x k_pad]
+  float* s1 = nullptr;       // [o] (this shard)
+  float* k = nullptr;        // [h]
+  size_t device_bytes = 0;
+  CUtensorMap tmA{};  // non-fused A operand
+  std::mutex ws_mu;
+  void* ws = nullptr;
+  size_t ws_cap = 0;
+};
+
+extern "C" {
+
+int dgq_abi_version(void) { return DGQ_B200_ABI_VERSION; }
+const char* dgq_last_error(void) { return t_msg.c_str(); }
+const char* dgq_last_error_field(void) { return t_field.c_str(); }
+
+dgq_status dgq_clip_interval(int s2, int zp, int* lo, int* hi) {
+  if (s2 < 1) return fail(DGQ_EINVAL, "clip_interval requires S2 >= 1");
+  const int a = (-127) / s2 + zp, b = 127 / s2 + zp;  // C++ truncating division
+  const int l = a > 0 ? a : 0, u = b < 15 ? b : 15;
+  if (l > u)
+    return fail(DGQ_EOVERFLOW, "empty clip interval for S2=" + std::to_string(s2) + " ZP=" + std::to_string(zp));
+  *lo = l;
+  *hi = u;
+  return DGQ_OK;
+}
+
+float dgq_fp16_round(float x) {
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  const uint32_t sign = b & 0x80000000u, mag = b & 0x7FFFFFFFu;
+  if (mag >= 0x7F800000u) return x;
+  const int e = static_cast<int>(mag >> 23) - 127;
+  uint32_t h;
+  if (e > 15) {
+    h = 0x7C00u;
+  } else if (e >= -14) {
+    const uint32_t m = mag & 0x7FFFFFu, rem = m & 0x1FFFu;
+    h = (static_cast<uint32_t>(e + 15) << 10) | (m >> 13);
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+  } else if (e >= -24) {
+    const uint32_t m = (mag & 0x7FFFFFu) | 0x800000u;
+    const int sh = -e - 1;
+    const uint32_t rem = m & ((1u << sh) - 1u), half = 1u << (sh - 1);
+    h = m >> sh;
+    if (rem > half || (rem == half && (h & 1u))) ++h;
+  } else {
+    h = 0;
+  }
+  const uint32_t he = (h >> 10) & 0x1Fu;
+  uint32_t hm = h & 0x3FFu, out;
+  if (he == 0x1Fu) {
+    out = sign | 0x7F800000u;
+  } else if (he) {
+    out = sign | ((he + 112u) << 23) | (hm << 13);
+  } else if (!hm) {
+    out = sign;
+  } else {
+    int sh = 0;
+    while (!(hm & 0x400u)) {
+      hm <<= 1;
+      --sh;
+    }
+    out = sign | (static_cast<uint32_t>(113 + sh) << 23) | ((hm & 0x3FFu) << 13);
+  }
+  float r;
+  std::memcpy(&r, &out, 4);
+  return r;
+}
+
+dgq_status dgq_validate_layer(size_t h, size_t o, size_t g, int mode, float act_scale, const uint8_t* codes,
+                              const int8_t* s2, const uint8_t* zp, const float* s1, const float* k) {
+  auto bad = [](const char* field, const std::string& m) {
+    return fail(DGQ_EVALIDATION, std::string("invalid DgqLayer field '") + field + "': " + m, field);
+  };
+  if (h == 0 || o == 0) return bad("shape", "h and o must be positive");
+  if (o % 2) return bad("shape", "o must be even for packed 4-bit storage");
+  if (g == 0 || h % g) return bad("g", "group size must divide h");
+  if (!codes || !s2 || !zp || !s1 || !k) return fail(DGQ_EINVAL, "null layer array");
+  const size_t ng = h / g;
+  for (size_t i = 0; i < ng * o; ++i)
+    if (s2[i] < 1) return bad("s2", "value " + std::to_string(int(s2[i])) + " outside [1, 127]");
+  for (size_t c = 0; c < o; ++c)
+    if (!(s1[c] > 0.0f) || !std::isfinite(s1[c])) return bad("s1", "scales must be positive and finite");
+  for (size_t j = 0; j < h; ++j)
+    if (!(k[j] >= 1.0f) || !std::isfinite(k[j])) return bad("k", "smoothing scales must be >= 1");
+  if (mode == DGQ_MODE_STATIC && !(act_scale > 0.0f))
+    return bad("act_scale", "static mode requires a positive activation scale");
+  if (!(act_scale >= 0.0f) || !std::isfinite(act_scale)) return bad("act_scale", "must be finite and non-negative");
+  for (size_t kk = 0; kk < ng; ++kk)
+    for (size_t c = 0; c < o; ++c) {
+      const int sv = s2[kk * o + c], z = nib(zp, kk * o + c);
+      const int q = 127 / sv;
+      const int lo = std::max(0, z - q), hi = std::min(15, z + q);
+      for (size_t j = 0; j < g; ++j) {
+        const size_t i = kk * g + j;
+        const int code = nib(codes, i * o + c);
+        if (code < lo || code > hi)
+          return bad("codes", "code " + std::to_string(code) + " at (" + std::to_string(i) + ", " +
+                                  std::to_string(c) + ") outside clip interval [" + std::to_string(lo) + ", " +
+                                  std::to_string(hi) + "]");
+      }
+    }
+  return DGQ_OK;
+}
+
+void dgq_layer_destroy(dgq_layer* L) {
+  if (!L) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(L->device);
+  cudaFree(L->tiles);
+  cudaFree(L->wt);
+  cudaFree(L->s1);
+  cudaFree(L->k);
+  cudaFree(L->ws);
+  cudaSetDevice(prev);
+  delete L;
+}
+
+dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, float act_scale,
+                            const uint8_t* codes, const int8_t* s2, const uint8_t* zp, const float* s1,
+                            const float* k, size_t col_begin, size_t col_end, int validate, void* stream,
+                            dgq_layer** out) {
+  if (!out) return fail(DGQ_EINVAL, "out is null");
+  *out = nullptr;
+  if (validate) {
+    dgq_status st = dgq_validate_layer(h, o, g, mode, act_scale, codes, s2, zp, s1, k);
+    if (st != DGQ_OK) return st;
+  } else if (h == 0 || o == 0 || o % 2 || g == 0 || h % g) {
+    return fail(DGQ_EINVAL, "inconsistent layer shape");
+  }
+  if (col_end == 0) col_end = o;
+  if (col_begin >= col_end || col_end > o) return fail(DGQ_EINVAL, "bad column shard range");
+  if (h > (1u << 30) || o > (1u << 30)) return fail(DGQ_EINVAL, "layer too large");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DGQ_CUDA(cudaSetDevice(device));
+
+  auto* L = new dgq_layer();
+  L->device = device;
+  L->h = h;
+  L->o_full = o;
+  L->c0 = col_begin;
+  L->o = col_end - col_begin;
+  L->g = g;
+  L->mode = mode ? DGQ_MODE_DYNAMIC : DGQ_MODE_STATIC;
+  L->act_scale = act_scale;
+  L->k_pad = round_up(h, 128);
+  L->n_pad = round_up(L->o, 128);
+  L->n_tiles = static_cast<int>(L->n_pad / 128);
+  L->k_blocks = static_cast<int>(L->k_pad / 128);
+  L->fused = dgq_layout::fused_ok(static_cast<int>(g));
+
+  const size_t ng = h / g;
+  const size_t codes_b = h * o / 2, s2_b = ng * o, zp_b = ng * o / 2;
+  uint8_t *d_codes = nullptr, *d_zp = nullptr;
+  int8_t* d_s2 = nullptr;
+  auto cleanup_tmp = [&] {
+    cudaFree(d_codes);
+    cudaFree(d_s2);
+    cudaFree(d_zp);
+  };
+#define DGQ_CUDA_L(expr)                        \
+  do {                                          \
+    cudaError_t e_ = (expr);                    \
+    if (e_ != cudaSuccess) {                    \
+      cleanup_tmp();                            \
+      dgq_layer_destroy(L);                     \
+      return fail(e_ == cudaErrorMemoryAllocation ? DGQ_ENOMEM : DGQ_ECUDA, \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    }                                           \
+  } while (0)
+  DGQ_CUDA_L(cudaMalloc(&d_codes, codes_b));
+  DGQ_CUDA_L(cudaMalloc(&d_s2, s2_b));
+  DGQ_CUDA_L(cudaMalloc(&d_zp, zp_b));
+  DGQ_CUDA_L(cudaMemcpyAsync(d_codes, codes, codes_b, cudaMemcpyHostToDevice, st));
+  DGQ_CUDA_L(cudaMemcpyAsync(d_s2, s2, s2_b, cudaMemcpyHostToDevice, st));
+  DGQ_CUDA_L(cudaMemcpyAsync(d_zp, zp, zp_b, cudaMemcpyHostToDevice, st));
+  DGQ_CUDA_L(cudaMalloc(&L->s1, L->o * sizeof(float)));
+  DGQ_CUDA_L(cudaMalloc(&L->k, h * sizeof(float)));
+  DGQ_CUDA_L(cudaMemcpyAsync(L->s1, s1 + col_begin, L->o * sizeof(float), cudaMemcpyHostToDevice, st));
+  DGQ_CUDA_L(cudaMemcpyAsync(L->k, k, h * sizeof(float), cudaMemcpyHostToDevice, st));
+  L->device_bytes = (L->o + h) * sizeof(float);
+  if (L->fused) {
+    const size_t tb = static_cast<size_t>(L->n_tiles) * L->k_blocks * dgq_layout::chunk_bytes(static_cast<int>(g));
+    DGQ_CUDA_L(cudaMalloc(&L->tiles, tb));
+    L->device_bytes += tb;
+    DGQ_CUDA_L(dgq_launch_repack(d_codes, d_s2, d_zp, static_cast<int>(h), static_cast<int>(o), static_cast<int>(g),
+                                 static_cast<int>(col_begin), static_cast<int>(L->o), L->n_tiles, L->k_blocks,
+                                 L->tiles, st));
+  } else {
+    // exotic group sizes: materialise W_s8 once, transpose to K-major
+    int8_t* w_full = nullptr;
+    unsigned long long* d_bad = nullptr;
+    DGQ_CUDA_L(cudaMalloc(&w_full, h * o));
+    DGQ_CUDA_L(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    DGQ_CUDA_L(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st));
+    DGQ_CUDA_L(dgq_launch_dequant_ref(d_codes, d_s2, d_zp, static_cast<int>(h), static_cast<int>(o),
+                                      static_cast<int>(g), w_full, d_bad, st));
+    // transpose the shard's columns
+    DGQ_CUDA_L(cudaMalloc(&L->wt, L->n_pad * L->k_pad));
+    L->device_bytes += L->n_pad * L->k_pad;
+    int8_t* w_shard = w_full;
+    if (L->o != o) {
+      DGQ_CUDA_L(cudaMalloc(&w_shard, h * L->o));
+      DGQ_CUDA_L(cudaMemcpy2DAsync(w_shard, L->o, w_full + col_begin, o, L->o, h, cudaMemcpyDeviceToDevice, st));
+    }
+    DGQ_CUDA_L(dgq_launch_transpose_pad(w_shard, static_cast<int>(h), static_cast<int>(L->o), L->wt,
+                                        static_cast<int>(L->k_pad), static_cast<int>(L->n_pad), st));
+    DGQ_CUDA_L(cudaStreamSynchronize(st));
+    if (w_shard != w_full) cudaFree(w_shard);
+    cudaFree(w_full);
+    cudaFree(d_bad);
+    dgq_status ms = make_tmap(&L->tmA, L->wt, L->n_pad, L->k_pad, L->k_pad, 128);
+    if (ms != DGQ_OK) {
+      cleanup_tmp();
+      dgq_layer_destroy(L);
+      return ms;
+    }
+  }
+  DGQ_CUDA_L(cudaStreamSynchronize(st));
+  cleanup_tmp();
+#undef DGQ_CUDA_L
+  *out = L;
+  return DGQ_OK;
+}
+
+dgq_status dgq_layer_create_from_dgq1(int device, const uint8_t* bytes, size_t nbytes, size_t col_begin,
+                                      size_t col_end, void* stream, dgq_layer** out) {
+  // DGQ1 layout, proj/include/dgq/format.hpp:6-21; checks of proj/src/format.cpp:214-250
+  constexpr size_t kHeader = 29;
+  if (!bytes || nbytes < kHeader) return fail(DGQ_EFORMAT, "truncated: DGQ file shorter than the header", "truncated");
+  if (std::memcmp(bytes, "DGQ1", 4) != 0) return fail(DGQ_EFORMAT, "bad magic, expected \"DGQ1\"", "bad_magic");
+  auto u64 = [&](size_t off) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(bytes[off + i]) << (8 * i);
+    return v;
+  };
+  const uint64_t h = u64(4), o = u64(12), g = u64(20);
+  const uint8_t mode = bytes[28];
+  if (mode > 1) return fail(DGQ_EFORMAT, "unknown mode byte " + std::to_string(int(mode)), "bad_header");
+  if (h == 0 || o == 0 || o % 2 || g == 0 || h % g)
+    return fail(DGQ_EFORMAT, "inconsistent dimensions in header", "bad_header");
+  if (h > (1ull << 30) || o > (1ull << 30)) return fail(DGQ_EFORMAT, "dimensions too large", "bad_header");
+  const uint64_t ng = h / g;
+  const uint64_t need = kHeader + h * o / 2 + ng * o + ng * o / 2 + 4 * o + 4 * h + 4;
+  if (nbytes < need) return fail(DGQ_EFORMAT, "truncated payload", "truncated");
+  if (nbytes > need) return fail(DGQ_EFORMAT, "payload longer than the header implies", "size_mismatch");
+  const uint8_t* p = bytes + kHeader;
+  const uint8_t* codes = p;
+  p += h * o / 2;
+  const int8_t* s2 = reinterpret_cast<const int8_t*>(p);
+  p += ng * o;
+  const uint8_t* zp = p;
+  p += ng * o / 2;
+  std::vector<float> s1(o), k(h);
+  std::memcpy(s1.data(), p, 4 * o);
+  p += 4 * o;
+  std::memcpy(k.data(), p, 4 * h);
+  p += 4 * h;
+  float act_scale;
+  std::memcpy(&act_scale, p, 4);
+  return dgq_layer_create(device, h, o, g, mode, act_scale, codes, s2, zp, s1.data(), k.data(), col_begin, col_end,
+                          1, stream, out);
+}
+
+dgq_status dgq_layer_get_info(const dgq_layer* L, dgq_layer_info* info) {
+  if (!L || !info) return fail(DGQ_EINVAL, "null argument");
+  info->h = L->h;
+  info->o_full = L->o_full;
+  info->o = L->o;
+  info->col_begin = L->c0;
+  info->g = L->g;
+  info->k_pad = L->k_pad;
+  info->n_pad = L->n_pad;
+  info->mode = L->mode;
+  info->act_scale = L->act_scale;
+  info->fused = L->fused ? 1 : 0;
+  info->device_bytes = L->device_bytes;
+  return DGQ_OK;
+}
+
+size_t dgq_linear_workspace_bytes(const dgq_layer* L, size_t M) {
+  if (!L || M == 0) return 0;
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), static_cast<int>(L->o), static_cast<int>(L->k_pad), L->fused,
+                                 static_cast<int>(L->g));
+  return pl.ws_bytes + pl.counter_bytes;
+}
+
+dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx, const float* dK, int mode,
+                                float act_scale, int8_t* dXq, size_t ldq, float* dRowScale, void* stream) {
+  if (M == 0) return DGQ_OK;
+  if (!dX || !dK || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
+  if (ldx < K || ldq < K) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
+  if (M > 0x7FFFFFFF || K > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too large");
+  DGQ_CUDA(dgq_launch_actquant(dX, ldx, dK, static_cast<int>(K), static_cast<int>(ldq), mode != 0, act_scale, dXq,
+                               ldq, dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream)));
+  return DGQ_OK;
+}
+
+dgq_status dgq_quantize_act(const dgq_layer* L, const float* dX, size_t M, size_t ldx, int8_t* dXq, size_t ldq,
+                            float* dRowScale, void* stream) {
+  if (!L) return fail(DGQ_EINVAL, "null layer");
+  return dgq_quantize_act_raw(dX, M, L->h, ldx, L->k, L->mode, L->act_scale, dXq, ldq, dRowScale, stream);
+}
+
+static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& tmA, int g, size_t N, size_t k_pad,
+                           const int8_t* dXq, size_t ldq, size_t M, const float* dRs, const float* dS1,
+                           const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
+                           size_t ld_acc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), static_cast<int>(N), static_cast<int>(k_pad), fused, g);
+  if (pl.ws_bytes + pl.counter_bytes > ws_bytes)
+    return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(pl.ws_bytes + pl.counter_bytes));
+  CUtensorMap tmB;
+  dgq_status ms = make_tmap(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn));
+  if (ms != DGQ_OK) return ms;
+  DgqGemmParams p{};
+  p.tiles = tiles;
+  p.chunk_bytes = static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128));
+  p.chunk_stride = (p.chunk_bytes + 1023u) & ~1023u;
+  p.gshift = 7;
+  if (g > 0 && g < 128) {
+    p.gshift = 0;
+    while ((1 << p.gshift) < g) ++p.gshift;
+  }
+  p.M = static_cast<int>(M);
+  p.N = static_cast<int>(N);
+  p.k_blocks = static_cast<int>(k_pad / 128);
+  p.kb_per_split = pl.kb_per_split;
+  p.splits = pl.splits;
+  p.rs = dRs;
+  p.s1 = dS1;
+  p.bias = dBias;
+  p.out = dY;
+  p.ldy = ldy;
+  p.out_f16 = out_dtype == DGQ_OUT_F16;
+  p.fp16_mode = fp16_mode;
+  p.acc_out = dAcc;
+  p.ld_acc = ld_acc;
+  if (pl.splits > 1) {
+    p.ws = static_cast<int32_t*>(ws);
+    p.ldw = static_cast<size_t>(pl.n_tiles) * 128;
+    p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
+  }
+  DGQ_CUDA(dgq_launch_gemm(pl, fused, tmB, tmA, p, st));
+  return DGQ_OK;
+}
+
+dgq_status dgq_linear(const dgq_layer* Lc, const int8_t* dXq, size_t ldq, const float* dRs, size_t M,
+                      const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
+                      size_t ld_acc, void* dWorkspace, size_t ws_bytes, void* stream) {
+  auto* L = const_cast<dgq_layer*>(Lc);
+  if (!L) return fail(DGQ_EINVAL, "null layer");
+  if (M == 0) return DGQ_OK;
+  if (!dXq || !dRs) return fail(DGQ_EINVAL, "null activation codes or row scales");
+  if (ldq != L->k_pad) return fail(DGQ_EINVAL, "ldq must equal the layer's k_pad (" + std::to_string(L->k_pad) + ")");
+  if (reinterpret_cast<uintptr_t>(dXq) % 16) return fail(DGQ_EINVAL, "activation codes must be 16-byte aligned");
+  if (dY && ldy < L->o) return fail(DGQ_EINVAL, "ldy smaller than the output width");
+  if (dAcc && ld_acc < L->o) return fail(DGQ_EINVAL, "ld_acc smaller than the output width");
+  if (M > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too many rows");
+  if (static_cast<double>(L->h) * 127.0 * 127.0 >= 2147483648.0)
+    return fail(DGQ_EINVAL, "h too large for 32-bit accumulation");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t need = dgq_linear_workspace_bytes(L, M);
+  void* ws = dWorkspace;
+  std::unique_lock<std::mutex> lk(L->ws_mu, std::defer_lock);
+  if (need && !ws) {
+    lk.lock();
+    if (L->ws_cap < need) {
+      cudaFree(L->ws);
+      L->ws = nullptr;
+      L->ws_cap = 0;
+      DGQ_CUDA(cudaMalloc(&L->ws, need));
+      DGQ_CUDA(cudaMemset(L->ws, 0, need));
+      L->ws_cap = need;
+    }
+    ws = L->ws;
+    ws_bytes = L->ws_cap;
+  }
+  return run_gemm(L->fused, L->tiles, L->tmA, static_cast<int>(L->g), L->o, L->k_pad, dXq, ldq, M, dRs, L->s1,
+                  dBias, out_dtype, fp16_mode, dY, ldy, dAcc, ld_acc, ws, ws_bytes, st);
+}
+
+dgq_status dgq_forward_device(const dgq_layer* L, const float* dX, size_t M, size_t ldx, const float* dBias,
+                              int out_dtype, void* dY, size_t ldy, int8_t* dXq, float* dRs, void* dWorkspace,
+                              size_t ws_bytes, void* stream) {
+  if (!L) return fail(DGQ_EINVAL, "null layer");
+  dgq_status s = dgq_quantize_act(L, dX, M, ldx, dXq, L->k_pad, dRs, stream);
+  if (s != DGQ_OK) return s;
+  return dgq_linear(L, dXq, L->k_pad, dRs, M, dBias, out_dtype, 0, dY, ldy, nullptr, 0, dWorkspace, ws_bytes,
+                    stream);
+}
+
+dgq_status dgq_layer_dequant_s8(const dgq_layer* L, int8_t* dW, size_t ldw, void* stream) {
+  if (!L || !dW) return fail(DGQ_EINVAL, "null argument");
+  if (ldw < L->o) return fail(DGQ_EINVAL, "ldw smaller than the shard width");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (L->fused) {
+    DGQ_CUDA(dgq_launch_dequant_tiles(L->tiles, static_cast<int>(L->g), static_cast<int>(L->h),
+                                      static_cast<int>(L->o), L->n_tiles, L->k_blocks, dW, ldw, st));
+  } else {
+    // transpose back from the K-major copy
+    DGQ_CUDA(dgq_launch_transpose_pad(L->wt, static_cast<int>(L->n_pad), static_cast<int>(L->k_pad), dW,
+                                      static_cast<int>(L->o), static_cast<int>(L->h), st));
+  }
+  return DGQ_OK;
+}
+
+dgq_status dgq_dequantize_to_s8(size_t h, size_t o, size_t g, const uint8_t* d_codes, const int8_t* d_s2,
+                                const uint8_t* d_zp, int8_t* dW, void* stream) {
+  if (h == 0 || o == 0 || o % 2 || g == 0 || h % g) return fail(DGQ_EINVAL, "inconsistent layer shape");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d_bad = nullptr;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(unsigned long long), st));
+  DGQ_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st));
+  DGQ_CUDA(dgq_launch_dequant_ref(d_codes, d_s2, d_zp, static_cast<int>(h), static_cast<int>(o), static_cast<int>(g),
+                                  dW, d_bad, st));
+  unsigned long long bad = 0;
+  DGQ_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  DGQ_CUDA(cudaFreeAsync(d_bad, st));
+  DGQ_CUDA(cudaStreamSynchronize(st));
+  if (bad != ~0ull) {
+    const size_t i = bad / o, c = bad % o;
+    return fail(DGQ_EVALIDATION,
+                "dequantized 8-bit weight at (" + std::to_string(i) + ", " + std::to_string(c) +
+                    ") outside [-127, 127]; artifact is corrupted",
+                "codes");
+  }
+  return DGQ_OK;
+}
+
+dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K,
+                                 size_t N, int64_t* max_abs_acc, void* stream) {
+  if (!max_abs_acc) return fail(DGQ_EINVAL, "null output");
+  *max_abs_acc = 0;
+  if (M == 0 || N == 0 || K == 0) return DGQ_OK;
+  if (M > 65535) return fail(DGQ_EINVAL, "audit supports at most 65535 rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), st));
+  DGQ_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+  DGQ_CUDA(dgq_launch_audit(dXq, ldx, dW, ldw, static_cast<int>(M), static_cast<int>(K), static_cast<int>(N), d, st));
+  unsigned long long v = 0;
+  DGQ_CUDA(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, st));
+  DGQ_CUDA(cudaFreeAsync(d, st));
+  DGQ_CUDA(cudaStreamSynchronize(st));
+  *max_abs_acc = static_cast<int64_t>(v);
+  return DGQ_OK;
+}
+
+dgq_status dgq_int8_gemm(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K, size_t N,
+                         int32_t* dAcc, size_t ld_acc, int64_t* max_abs_acc, void* stream) {
+  if (static_cast<double>(K) * 127.0 * 127.0 >= 2147483648.0)
+    return fail(DGQ_EINVAL, "h too large for 32-bit accumulation");
+  if (max_abs_acc) *max_abs_acc = 0;
+  if (M == 0 || N == 0) return DGQ_OK;
+  if (!dXq || !dW || !dAcc) return fail(DGQ_EINVAL, "null argument");
+  if (ldx < K || ldw < N || ld_acc < N) return fail(DGQ_EINVAL, "leading dimension too small");
+  if (M > 0x7FFFFFFF || N > (1u << 30)) return fail(DGQ_EINVAL, "too large");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t k_pad = round_up(K ? K : 1, 128), n_pad = round_up(N, 128);
+  int8_t *wt = nullptr, *xq = nullptr;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wt), n_pad * k_pad, st));
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xq), M * k_pad, st));
+  // W [K x N] (ld = ldw) -> WT [n_pad x k_pad]
+  const int8_t* wsrc = dW;
+  int8_t* wdense = nullptr;
+  if (ldw != N) {
+    DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wdense), K * N ? K * N : 1, st));
+    DGQ_CUDA(cudaMemcpy2DAsync(wdense, N, dW, ldw, N, K, cudaMemcpyDeviceToDevice, st));
+    wsrc = wdense;
+  }
+  DGQ_CUDA(dgq_launch_transpose_pad(wsrc, static_cast<int>(K), static_cast<int>(N), wt, static_cast<int>(k_pad),
+                                    static_cast<int>(n_pad), st));
+  DGQ_CUDA(cudaMemsetAsync(xq, 0, M * k_pad, st));
+  if (K) DGQ_CUDA(cudaMemcpy2DAsync(xq, k_pad, dXq, ldx, K, M, cudaMemcpyDeviceToDevice, st));
+  CUtensorMap tmA;
+  dgq_status s = make_tmap(&tmA, wt, n_pad, k_pad, k_pad, 128);
+  void* ws = nullptr;
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), static_cast<int>(N), static_cast<int>(k_pad), false, 128);
+  const size_t need = pl.ws_bytes + pl.counter_bytes;
+  if (s == DGQ_OK && need) {
+    DGQ_CUDA(cudaMallocAsync(&ws, need, st));
+    DGQ_CUDA(cudaMemsetAsync(ws, 0, need, st));
+  }
+  if (s == DGQ_OK)
+    s = run_gemm(false, nullptr, tmA, 128, N, k_pad, xq, k_pad, M, nullptr, nullptr, nullptr, DGQ_OUT_F32, 0, nullptr,
+                 0, dAcc, ld_acc, ws, need, st);
+  if (s == DGQ_OK && max_abs_acc) s = dgq_audit_max_abs_acc(dXq, ldx, dW, ldw, M, K, N, max_abs_acc, stream);
+  if (ws) cudaFreeAsync(ws, st);
+  if (wdense) cudaFreeAsync(wdense, st);
+  cudaFreeAsync(wt, st);
+  cudaFreeAsync(xq, st);
+  if (s == DGQ_OK && max_abs_acc && *max_abs_acc > 2147483647LL)
+    return fail(DGQ_EOVERFLOW, "int8_gemm accumulator overflow despite precondition");
+  return s;
+}
+
+dgq_status dgq_epilogue(const int32_t* dAcc, size_t lda, const float* dRs, const float* dS1, const float* dBias,
+                        size_t M, size_t N, int fp16_mode, int out_dtype, void* dY, size_t ldy, void* stream) {
+  if (M == 0 || N == 0) return DGQ_OK;
+  if (!dAcc || !dRs || !dS1 || !dY) return fail(DGQ_EINVAL, "null argument");
+  if (lda < N || ldy < N) return fail(DGQ_EINVAL, "leading dimension too small");
+  DGQ_CUDA(dgq_launch_epilogue(dAcc, lda, dRs, dS1, dBias, static_cast<int>(M), static_cast<int>(N), fp16_mode,
+                               out_dtype == DGQ_OUT_F16, dY, ldy, static_cast<cudaStream_t>(stream)));
+  return DGQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// Internal launch interface between the C-ABI layer (capi.cu) and the kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+// ---- prepared ("B200-tiled") weight layout ---------------------------------
+// Output channels are cut into 128-row tiles, the reduction axis into 128-wide
+// k-blocks.  Every (n-tile, k-block) owns one contiguous chunk in HBM:
+//   [0, 8192)            packed INT4 codes: for j in 0..3 (32-k slice), for n in
+//                        0..127: 16 B = 4 words of 8 k each.  Inside a word the
+//                        k-offset t sits in nibble kNibblePos[t], the order the
+//                        in-kernel IMAD/PRMT dequantiser emits bytes in.
+//   [8192, 8192+256*gpk) per-group scales: for each group overlapping the
+//                        k-block, 128 x u16 (S2 | ZP << 8).
+// Chunks are ordered n-tile major so one CTA streams a contiguous range.
+namespace dgq_layout {
+constexpr int kTileN = 128;
+constexpr int kBlockK = 128;
+constexpr int kCodeBytes = 8192;
+constexpr int kNibblePos[8] = {0, 1, 4, 5, 2, 3, 6, 7};
+inline int groups_per_kblock(int g) { return g >= kBlockK ? 1 : kBlockK / g; }
+inline int chunk_bytes(int g) { return kCodeBytes + 256 * groups_per_kblock(g); }
+// The fused path needs every 8-k word inside one group and whole groups per
+// k-block (or whole k-blocks per group).
+inline bool fused_ok(int g) {
+  return g > 0 && g % 8 == 0 && ((kBlockK % g == 0) || (g % kBlockK == 0));
+}
+}  // namespace dgq_layout
+
+struct DgqGemmParams {
+  // A side (weights): prepared INT4 tiles (fused) or via tensor map (plain int8)
+  const uint8_t* tiles;
+  uint32_t chunk_bytes;
+  uint32_t chunk_stride;  // smem bytes per staged chunk
+  uint32_t gshift;        // k-offset >> gshift = group index inside a k-block
+  int M, N, k_blocks, kb_per_split, splits;
+  // epilogue
+  const float* rs;    // [M] per-token scales
+  const float* s1;    // [N] per-channel scales (may be null when out == null)
+  const float* bias;  // [N] or null
+  void* out;          // [M x ldy] f32 or f16, or null
+  size_t ldy;
+  int out_f16;
+  int fp16_mode;
+  int32_t* acc_out;  // optional raw int32 accumulators [M x ld_acc]
+  size_t ld_acc;
+  // split-K workspace (zero on entry, left zero on exit)
+  int32_t* ws;
+  size_t ldw;
+  uint32_t* counters;
+};
+
+struct DgqGemmPlan {
+  int bn;
+  int m_tiles, n_tiles, splits, kb_per_split;
+  size_t smem_bytes;
+  size_t ws_bytes;       // split-K accumulator bytes needed (0 if splits == 1)
+  size_t counter_bytes;  // split-K tile counters
+};
+
+DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn = 0, int force_splits = 0);
+
+cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorMap& tmB, const CUtensorMap& tmA,
+                            const DgqGemmParams& p, cudaStream_t st);
+
+cudaError_t dgq_launch_actquant(const float* X, size_t ldx, const float* k, int K, int Kpad, int dynamic,
+                                float act_scale, int8_t* Q, size_t ldq, float* rs, int M, cudaStream_t st);
+
+// Reference layout (codes u4 [h x o_full] packed along o, s2 i8, zp u4) column
+// slice [c0, c0+n) -> prepared tiles.
+cudaError_t dgq_launch_repack(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int h, int o_full, int g,
+                              int c0, int n, int n_tiles, int k_blocks, uint8_t* tiles, cudaStream_t st);
+// prepared tiles -> W_s8 row-major [h x n] (same dequantiser as the fused GEMM)
+cudaError_t dgq_launch_dequant_tiles(const uint8_t* tiles, int g, int h, int n, int n_tiles, int k_blocks,
+                                     int8_t* w, size_t ldw, cudaStream_t st);
+// Reference layout -> W_s8 row-major [h x o]; flags any value outside [-127,127]
+// (first offending linear index in *bad, initialised to UINT64_MAX).
+cudaError_t dgq_launch_dequant_ref(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int h, int o, int g,
+                                   int8_t* w, unsigned long long* bad, cudaStream_t st);
+// W [K x N] row-major -> WT [Npad x Kpad] K-major, zero padded.
+cudaError_t dgq_launch_transpose_pad(const int8_t* W, int K, int N, int8_t* WT, int Kpad, int Npad, cudaStream_t st);
+// Standalone epilogue over an int32 accumulator [M x N] (ld = N).
+cudaError_t dgq_launch_epilogue(const int32_t* acc, size_t lda, const float* rs, const float* s1, const float* bias,
+                                int M, int N, int fp16_mode, int out_f16, void* y, size_t ldy, cudaStream_t st);
+// max over (r, c, i) of |prefix sum| (proj/src/kernel.cpp:73-77); *out must be 0.
+cudaError_t dgq_launch_audit(const int8_t* Xq, size_t ldx, const int8_t* W, size_t ldw, int M, int K, int N,
+                             unsigned long long* out, cudaStream_t st);

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden vectors.  Integer stages and the FP32 epilogue are
+bit-exact; FP16 outputs equal fp16_round(FP32 reference) bit-exactly, which
+implies |y16 - y| <= 2^-11 |y| + 2^-24 (the stated FP16 tolerance)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2310_04836_b200 as dgq
+
+pytestmark = pytest.mark.gpu
+
+
+def _to_dgq(L: oracle.Layer) -> dgq.DgqLayer:
+    return dgq.DgqLayer(h=L.h, o=L.o, g=L.g, codes=L.codes.copy(), s2=np.asarray(L.s2).copy(), zp=L.zp.copy(),
+                        s1=L.s1.copy(), k=L.k.copy(), act_scale=L.act_scale, mode=L.mode)
+
+
+def _golden_layer(golden, p) -> dgq.DgqLayer:
+    o, h = int(golden[f"{p}.o"]), int(golden[f"{p}.h"])
+    return dgq.DgqLayer(h=h, o=o, g=int(golden[f"{p}.g"]), codes=golden[f"{p}.codes"], s2=golden[f"{p}.s2"],
+                        zp=golden[f"{p}.zp"], s1=golden.get(f"{p}.s1", np.ones(o, np.float32)),
+                        k=golden.get(f"{p}.k", np.ones(h, np.float32)),
+                        act_scale=float(golden.get(f"{p}.act_scale", 0.0)), mode=int(golden.get(f"{p}.mode", 1)))
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+# ------------------------------------------------------------------ goldens
+@pytest.mark.parametrize("case,mode", [("actq_dyn", 1), ("actq_odd", 1), ("actq_edge", 1), ("actq_static", 0)])
+def test_actq_golden(cuda, golden, case, mode):
+    X, k = golden[f"{case}.X"], golden[f"{case}.k"]
+    L = dgq.DgqLayer(h=X.shape[1], o=2, g=X.shape[1], codes=np.zeros(X.shape[1], np.uint8),
+                     s2=np.ones((1, 2), np.int8), zp=np.zeros(1, np.uint8), s1=np.ones(2, np.float32), k=k,
+                     act_scale=float(golden.get(f"{case}.act_scale", 0.0)), mode=mode)
+    aq = dgq.quantize_activations(X, L)
+    assert np.array_equal(aq.codes, golden[f"{case}.codes"])
+    assert np.array_equal(bits(aq.row_scales), bits(golden[f"{case}.rs"]))
+
+
+@pytest.mark.parametrize("case", ["deq_g64", "deq_g128", "deq_g8", "deq_g12"])
+def test_dequant_golden(cuda, golden, case):
+    L = _golden_layer(golden, case)
+    assert np.array_equal(dgq.dequantize_to_s8(L), golden[f"{case}.w_s8"])
+    CL = dgq.CudaLayer(L)  # prepared tiles (fused) or materialised (g=12)
+    assert np.array_equal(CL.dequant_s8().cpu().numpy(), golden[f"{case}.w_s8"])
+
+
+@pytest.mark.parametrize("case", ["gemm_16x64x8", "gemm_9x33x7", "gemm_40x300x130", "gemm_all127"])
+def test_int8_gemm_golden(cuda, golden, case):
+    r = dgq.int8_gemm(golden[f"{case}.Xq"], golden[f"{case}.Wq"])
+    assert np.array_equal(r.acc, golden[f"{case}.acc"])
+    assert r.max_abs_acc == int(golden[f"{case}.max_abs_acc"])
+
+
+def test_epilogue_golden(cuda, golden):
+    a, rs, s1, b = (golden[f"epi.{n}"] for n in ("acc", "rs", "s1", "bias"))
+    for fp16, bias, key in [(False, None, "y"), (False, b, "y_bias"), (True, None, "y_f16mode"),
+                            (True, b, "y_f16mode_bias")]:
+        y = dgq.epilogue(a, rs, s1, bias, fp16)
+        assert np.array_equal(bits(y), bits(golden[f"epi.{key}"])), key
+
+
+@pytest.mark.parametrize("case", ["fwd_a", "fwd_b"])
+def test_forward_golden(cuda, golden, case):
+    L = _golden_layer(golden, case)
+    bias = golden.get(f"{case}.bias")
+    fw = dgq.dgq_forward(golden[f"{case}.X"], L, bias)
+    assert np.array_equal(fw.w_s8, golden[f"{case}.w_s8"])
+    assert np.array_equal(fw.act.codes, golden[f"{case}.act_codes"])
+    assert np.array_equal(bits(fw.act.row_scales), bits(golden[f"{case}.rs"]))
+    assert np.array_equal(bits(fw.out), bits(golden[f"{case}.out"]))
+    assert fw.max_abs_acc == int(golden[f"{case}.max_abs_acc"])
+
+
+# ------------------------------------------------------- reference-test KATs
+def test_identity_coded_activations_select_rows(cuda):
+    # proj/tests/test_kernel.cpp:63-71
+    Xq = np.eye(3, dtype=np.int8)
+    Wq = np.random.default_rng(2).integers(-127, 128, (3, 5)).astype(np.int8)
+    assert np.array_equal(dgq.int8_gemm(Xq, Wq).acc, Wq.astype(np.int32))
+
+
+def test_hand_product(cuda):
+    # proj/tests/test_kernel.cpp:73-78
+    r = dgq.int8_gemm(np.array([[3, -4]], np.int8), np.array([[2], [5]], np.int8))
+    assert r.acc[0, 0] == -14
+
+
+def test_epilogue_kats(cuda):
+    # proj/tests/test_kernel.cpp:103-120
+    acc = np.array([[1, -5], [100000, 0]], np.int32)
+    assert np.array_equal(dgq.epilogue(acc, [1, 1], [1, 1]), acc.astype(np.float32))
+    assert dgq.epilogue(np.array([[6]], np.int32), [0.5], [0.25])[0, 0] == 0.75
+    y = dgq.epilogue(np.array([[10, 20]], np.int32), [0.1], [1, 1], [5.0, -1.0])
+    assert abs(y[0, 0] - 6.0) < 1e-5 and abs(y[0, 1] - 1.0) < 1e-5
+    with pytest.raises(dgq.InvalidArgument):
+        dgq.epilogue(acc, [1.0], [1.0, 1.0])
+
+
+def test_act_quant_kats(cuda):
+    # proj/tests/test_kernel.cpp:146-162
+    L = dgq.random_layer(2, 2, 2, 12)
+    L.k = np.ones(2, np.float32)
+    aq = dgq.quantize_activations(np.array([[-1.0, 1.0]], np.float32), L)
+    assert list(aq.codes[0]) == [-127, 127]
+    assert abs(aq.row_scales[0] - 1 / 127) < 1e-9
+    L4 = dgq.random_layer(4, 2, 4, 13)
+    aq = dgq.quantize_activations(np.zeros((1, 4), np.float32), L4)
+    assert aq.row_scales[0] == np.float32(1e-8) and not aq.codes.any()
+
+
+def test_corrupted_layer_dequant_raises(cuda):
+    # proj/tests/test_format.cpp:160-177
+    codes = np.array([[0, 1], [2, 3], [4, 5], [6, 7]], np.uint8)
+    L = dgq.DgqLayer(h=4, o=2, g=4, codes=dgq.pack_u4(codes), s2=np.array([[16, 16]], np.int8),
+                     zp=dgq.pack_u4([0, 0]), s1=np.array([0.01, 0.01], np.float32), k=np.ones(4, np.float32),
+                     act_scale=0.1, mode=1)
+    assert dgq.dequantize_to_s8(L)[3, 1] == 112
+    codes[3, 1] = 8
+    L.codes = dgq.pack_u4(codes)
+    with pytest.raises(dgq.ValidationError) as e:
+        dgq.dequantize_to_s8(L)
+    assert e.value.field == "codes"
+
+
+def test_h_too_large_rejected(cuda):
+    with pytest.raises(dgq.InvalidArgument):
+        dgq.int8_gemm(np.zeros((1, 140000), np.int8), np.zeros((140000, 2), np.int8))
+
+
+# ------------------------------------------------------------ random vs oracle
+@pytest.mark.parametrize("M,K,mode", [(1, 4096, 1), (7, 33, 1), (64, 1000, 1), (300, 4096, 1), (5, 28672, 1),
+                                      (3, 12288, 0), (33, 8192, 1), (2, 20000, 1)])
+def test_actq_random(cuda, port, M, K, mode):
+    X = port.gen_synthetic(M, K, 1000 + K, 3, 50.0, 7)
+    k = np.random.default_rng(K).uniform(1, 4, K).astype(np.float32)
+    act = float(np.abs(X / k).max() / 127.0 * 0.9)
+    q, rs = port.quantize_activations(X, k, mode, act)
+    L = dgq.DgqLayer(h=K, o=2, g=K, codes=np.zeros(K, np.uint8), s2=np.ones((1, 2), np.int8),
+                     zp=np.zeros(1, np.uint8), s1=np.ones(2, np.float32), k=k, act_scale=act, mode=mode)
+    aq = dgq.quantize_activations(X, L)
+    assert np.array_equal(aq.codes, q)
+    assert np.array_equal(bits(aq.row_scales), bits(rs))
+
+
+def test_actq_ties_exhaustive(cuda, port):
+    # every half-integer quotient (n + 1/2) * s for a spread of scales: ties must go to even
+    rows = []
+    for e in (-20, -7, 0, 5, 30):
+        s = np.float32(2.0 ** e * 1.2345)
+        vals = ((np.arange(-127, 127) + 0.5) * np.float64(s)).astype(np.float32)
+        row = np.concatenate([vals, [np.float32(127 * s)]]).astype(np.float32)
+        rows.append(row)
+    X = np.stack(rows)
+    k = np.ones(X.shape[1], np.float32)
+    q, rs = port.quantize_activations(X, k, 1, 0.0)
+    L = dgq.DgqLayer(h=X.shape[1], o=2, g=X.shape[1], codes=np.zeros(X.shape[1], np.uint8),
+                     s2=np.ones((1, 2), np.int8), zp=np.zeros(1, np.uint8), s1=np.ones(2, np.float32), k=k, mode=1)
+    aq = dgq.quantize_activations(X, L)
+    assert np.array_equal(aq.codes, q)
+
+
+@pytest.mark.parametrize("h,o,g", [(256, 64, 8), (512, 96, 16), (384, 256, 32), (1024, 200, 64), (4096, 130, 128),
+                                   (768, 64, 256), (96, 12, 24), (48, 10, 12), (4, 2, 4)])
+def test_prepared_dequant_matches_oracle(cuda, port, h, o, g):
+    L = oracle.random_layer(h, o, g, seed=h * 7 + g)
+    w = port.dequantize_to_s8(L)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    assert CL.fused == (g % 8 == 0 and (128 % g == 0 or g % 128 == 0))
+    assert np.array_equal(CL.dequant_s8().cpu().numpy(), w)
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 128, 128), (16, 4096, 512), (100, 1000, 300), (257, 512, 256), (513, 384, 130),
+                                   (2048, 1024, 256)])
+def test_int8_gemm_random(cuda, M, K, N):
+    rng = np.random.default_rng(M + K + N)
+    A = rng.integers(-127, 128, (M, K)).astype(np.int8)
+    B = rng.integers(-127, 128, (K, N)).astype(np.int8)
+    r = dgq.int8_gemm(A, B)
+    ref = (torch.from_numpy(A).double().cuda() @ torch.from_numpy(B).double().cuda()).round().long().cpu().numpy()
+    assert np.array_equal(r.acc.astype(np.int64), ref)
+
+
+FWD_CASES = [
+    # (M, h, o, g, mode)
+    (1, 4096, 512, 128, 1),
+    (16, 4096, 1024, 128, 1),
+    (16, 1024, 256, 64, 0),
+    (9, 96, 12, 24, 1),      # non-fused group size
+    (33, 512, 384, 32, 1),
+    (64, 2048, 256, 8, 1),
+    (100, 768, 300, 256, 1),
+    (300, 1024, 512, 128, 1),
+    (257, 256, 1000, 64, 0),
+]
+
+
+@pytest.mark.parametrize("M,h,o,g,mode", FWD_CASES)
+def test_fused_linear_matches_oracle(cuda, port, M, h, o, g, mode):
+    L = oracle.random_layer(h, o, g, seed=M * 31 + h + o, mode=mode)
+    calib = port.gen_synthetic(32, h, 7, 3, 50.0, 3)
+    L.k, _ = port.smooth_from_calib(calib)
+    L.act_scale = float(np.abs(calib / L.k).max() / 127.0)
+    X = port.gen_synthetic(M, h, 99 + M, 3, 50.0, 3)
+    bias = np.random.default_rng(M).uniform(-0.5, 0.5, o).astype(np.float32)
+    out, w, q, rs, mx = port.dgq_forward(X, L, bias)
+    D = _to_dgq(L)
+    CL = dgq.CudaLayer(D)
+    x = torch.from_numpy(X).cuda()
+    codes, drs = CL.quantize_act(x)
+    assert np.array_equal(codes[:, :h].cpu().numpy(), q)
+    assert not codes[:, h:].any()
+    assert np.array_equal(bits(drs.cpu().numpy()), bits(rs))
+    db = torch.from_numpy(bias).cuda()
+    y32, acc = CL.linear(codes, drs, bias=db, out_dtype=torch.float32, want_acc=True)
+    acc_ref, _ = port.int8_gemm(q, w)
+    assert np.array_equal(acc.cpu().numpy(), acc_ref)
+    assert np.array_equal(bits(y32.cpu().numpy()), bits(out))
+    y16 = CL.linear(codes, drs, bias=db, out_dtype=torch.float16)
+    ref16 = port.fp16_round_array(out).astype(np.float16)
+    assert np.array_equal(bits(y16.cpu().numpy()), bits(ref16))
+    # stated FP16 tolerance, implied by the bit-exact check above
+    d = np.abs(y16.cpu().numpy().astype(np.float64) - out.astype(np.float64))
+    assert (d <= np.abs(out) * 2.0 ** -11 + 2.0 ** -24 + 1e-30).all()
+
+
+def test_fp16_mode_epilogue_in_fused_kernel(cuda, port):
+    L = oracle.random_layer(512, 256, 128, seed=3)
+    X = port.gen_synthetic(20, 512, 5, 3, 50.0, 3)
+    out, w, q, rs, mx = port.dgq_forward(X, L)
+    acc, _ = port.int8_gemm(q, w)
+    ref = port.epilogue(acc, rs, L.s1, None, True)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+    y = CL.linear(codes, drs, out_dtype=torch.float32, fp16_mode=True)
+    assert np.array_equal(bits(y.cpu().numpy()), bits(ref))
+
+
+@pytest.mark.parametrize("M", [1, 4, 16, 48])
+def test_split_k_is_exact_and_workspace_reusable(cuda, port, M):
+    # decode shapes run split-K through the int32 workspace; run twice to check it is left zeroed
+    L = oracle.random_layer(4096, 256, 128, seed=M)
+    X = port.gen_synthetic(M, 4096, M, 3, 50.0, 3)
+    out, w, q, rs, mx = port.dgq_forward(X, L)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    assert dgq.lib().dgq_linear_workspace_bytes(CL.handle, M) > 0
+    codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+    for _ in range(3):
+        y = CL.linear(codes, drs, out_dtype=torch.float32)
+        assert np.array_equal(bits(y.cpu().numpy()), bits(out))
+
+
+def test_column_shards_concatenate_to_full(cuda, port):
+    L = oracle.random_layer(1024, 768, 128, seed=77)
+    X = port.gen_synthetic(40, 1024, 1, 3, 50.0, 3)
+    out, *_ = port.dgq_forward(X, L)
+    D = _to_dgq(L)
+    x = torch.from_numpy(X).cuda()
+    parts = []
+    for r in range(4):
+        c0, c1 = r * 192, (r + 1) * 192
+        S = dgq.CudaLayer(D, col_begin=c0, col_end=c1)
+        assert S.o == 192
+        parts.append(S.forward(x, out_dtype=torch.float32).cpu().numpy())
+    assert np.array_equal(bits(np.concatenate(parts, axis=1)), bits(out))
+
+
+def test_dgq1_to_device_layer(cuda, golden, port):
+    raw = golden["dgq1.bytes"].tobytes()
+    CL = dgq.CudaLayer.from_dgq1(raw)
+    L = dgq.layer_from_bytes(raw)
+    assert (CL.h, CL.o) == (L.h, L.o)
+    assert np.array_equal(CL.dequant_s8().cpu().numpy(), golden["dgq1.w_s8"] if "dgq1.w_s8" in golden else
+                          dgq.dequantize_to_s8(L))
+    with pytest.raises(dgq.FormatError):
+        dgq.CudaLayer.from_dgq1(raw[:-3])
+
+
+def test_max_accumulator_at_k28672(cuda):
+    # SURVEY.md §8d edge: all +127 activations against W_s8 == +127 at K = 28672
+    K, N = 28672, 256
+    codes = np.full((K, N), 1, np.uint8)
+    L = dgq.DgqLayer(h=K, o=N, g=128, codes=dgq.pack_u4(codes), s2=np.full((K // 128, N), 127, np.int8),
+                     zp=dgq.pack_u4(np.zeros((K // 128, N), np.uint8)), s1=np.ones(N, np.float32),
+                     k=np.ones(K, np.float32), act_scale=1.0, mode=0)
+    CL = dgq.CudaLayer(L)
+    x = torch.full((3, K), 1000.0, device="cuda")
+    codes_, rs = CL.quantize_act(x)
+    assert int(codes_[:, :K].min()) == 127
+    _, acc = CL.linear(codes_, rs, out_dtype=torch.float32, want_acc=True)
+    assert int(acc.min()) == int(acc.max()) == 28672 * 127 * 127 == 462_450_688
