@@ -98,6 +98,11 @@ dgq_status dgq_layer_get_info(const dgq_layer* layer, dgq_layer_info* info);
  * workspace is left zeroed on return, so it can be reused call after call. */
 size_t dgq_linear_workspace_bytes(const dgq_layer* layer, size_t M);
 
+/* The launch plan dgq_linear uses for M tokens: token-tile width, weight tiles
+ * per CTA, K splits (a thread-block cluster when > 1) and the CTA count. */
+dgq_status dgq_linear_plan(const dgq_layer* layer, size_t M, int* token_tile, int* weight_tiles, int* k_splits,
+                           int* ctas);
+
 /* ---- K1: per-token INT8 activation quantisation ----------------------------
  * replaces dgq::quantize_activations, proj/src/kernel.cpp:14-44.
  * dXq rows use stride ldq >= h (pass info.k_pad for dgq_linear); pad columns

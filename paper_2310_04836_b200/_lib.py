@@ -68,6 +68,7 @@ _SIGS = {
     "dgq_layer_destroy": (None, [_vp]),
     "dgq_layer_get_info": (_i, [_vp, C.POINTER(LayerInfo)]),
     "dgq_linear_workspace_bytes": (_sz, [_vp, _sz]),
+    "dgq_linear_plan": (_i, [_vp, _sz, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "dgq_quantize_act": (_i, [_vp, _vp, _sz, _sz, _vp, _sz, _vp, _vp]),
     "dgq_quantize_act_raw": (_i, [_vp, _sz, _sz, _sz, _vp, _i, _f, _vp, _sz, _vp, _vp]),
     "dgq_linear": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _i, _vp, _sz, _vp, _sz, _vp, _sz, _vp]),

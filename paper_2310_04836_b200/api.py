@@ -190,6 +190,12 @@ class CudaLayer:
     def handle(self):
         return self._h
 
+    def plan(self, M: int) -> dict:
+        """The kernel launch plan for M tokens (token tile, weight tiles per CTA, K splits, CTAs)."""
+        v = [C.c_int() for _ in range(4)]
+        check(lib().dgq_linear_plan(self._h, M, *[C.byref(x) for x in v]))
+        return dict(token_tile=v[0].value, weight_tiles=v[1].value, k_splits=v[2].value, ctas=v[3].value)
+
     def workspace(self, M: int) -> torch.Tensor | None:
         need = lib().dgq_linear_workspace_bytes(self._h, M)
         if need == 0:

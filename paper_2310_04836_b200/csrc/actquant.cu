@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(T) k_actquant_vec(const float* __restrict__ X,
                                                      int dynamic, float act_scale, int8_t* __restrict__ Q,
                                                      size_t ldq, float* __restrict__ rs, int M) {
   __shared__ float red[33];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // let the GEMM start streaming weights
   const int K4 = K >> 2;
   for (int row = blockIdx.x; row < M; row += gridDim.x) {
     const float4* xr = reinterpret_cast<const float4*>(X + static_cast<size_t>(row) * ldx);
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(T) k_actquant_any(const float* __restrict__ X,
                                                      int dynamic, float act_scale, int8_t* __restrict__ Q,
                                                      size_t ldq, float* __restrict__ rs, int M) {
   __shared__ float red[33];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int row = blockIdx.x; row < M; row += gridDim.x) {
     const float* xr = X + static_cast<size_t>(row) * ldx;
     float s = act_scale;

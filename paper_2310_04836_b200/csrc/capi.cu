@@ -66,6 +66,25 @@ dgq_status make_tmap(CUtensorMap* m, const void* base, size_t rows, size_t cols,
   return DGQ_OK;
 }
 
+unsigned long long* g_dbg_ts = nullptr;  // tools only: per-CTA phase timestamps
+
+// Output tensor map for the prefill epilogue: rows x cols elements of `dt`,
+// box = 32 rows x 128 bytes, 128-byte swizzle (matches the smem staging).
+dgq_status make_out_tmap(CUtensorMap* m, void* base, size_t rows, size_t cols, size_t ld, bool f16) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const size_t esz = f16 ? 2 : 4;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32u};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled (output) failed (" + std::to_string(r) + ")");
+  return DGQ_OK;
+}
+
 size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
 
 inline int nib(const uint8_t* p, size_t idx) { return (idx & 1) ? (p[idx >> 1] >> 4) : (p[idx >> 1] & 0x0F); }
@@ -94,6 +113,8 @@ struct dgq_layer {
 extern "C" {
 
 int dgq_abi_version(void) { return DGQ_B200_ABI_VERSION; }
+/* not in the public header: profiling hook for tools/ (device buffer of [cta][8] u64, or NULL) */
+void dgq_debug_set_timestamps(void* d_buf) { g_dbg_ts = static_cast<unsigned long long*>(d_buf); }
 const char* dgq_last_error(void) { return t_msg.c_str(); }
 const char* dgq_last_error_field(void) { return t_field.c_str(); }
 
@@ -370,6 +391,18 @@ size_t dgq_linear_workspace_bytes(const dgq_layer* L, size_t M) {
   return pl.ws_bytes + pl.counter_bytes;
 }
 
+dgq_status dgq_linear_plan(const dgq_layer* L, size_t M, int* token_tile, int* weight_tiles, int* k_splits,
+                           int* ctas) {
+  if (!L || M == 0) return fail(DGQ_EINVAL, "null layer or M == 0");
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), static_cast<int>(L->o), static_cast<int>(L->k_pad), L->fused,
+                                 static_cast<int>(L->g));
+  if (token_tile) *token_tile = pl.bn;
+  if (weight_tiles) *weight_tiles = pl.nt;
+  if (k_splits) *k_splits = pl.splits;
+  if (ctas) *ctas = pl.m_tiles * ((pl.n_tiles + pl.nt - 1) / pl.nt) * pl.splits;
+  return DGQ_OK;
+}
+
 dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx, const float* dK, int mode,
                                 float act_scale, int8_t* dXq, size_t ldq, float* dRowScale, void* stream) {
   if (M == 0) return DGQ_OK;
@@ -420,12 +453,22 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
   p.fp16_mode = fp16_mode;
   p.acc_out = dAcc;
   p.ld_acc = ld_acc;
-  if (pl.splits > 1) {
-    p.ws = static_cast<int32_t*>(ws);
-    p.ldw = static_cast<size_t>(pl.n_tiles) * 128;
-    p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
+  {
+    const size_t esz = out_dtype == DGQ_OUT_F16 ? 2 : 4;
+    bool ok = true;
+    if (dY) ok = ok && (reinterpret_cast<uintptr_t>(dY) % 16 == 0) && ((ldy * esz) % 16 == 0);
+    if (dAcc) ok = ok && (reinterpret_cast<uintptr_t>(dAcc) % 16 == 0) && ((ld_acc * 4) % 16 == 0);
+    p.vec_ok = ok ? 1 : 0;
   }
-  DGQ_CUDA(dgq_launch_gemm(pl, fused, tmB, tmA, p, st));
+  (void)ws;
+  CUtensorMap tmY{};
+  if (pl.bn >= 128 && dY && p.vec_ok) {
+    dgq_status ys = make_out_tmap(&tmY, dY, M, N, ldy, out_dtype == DGQ_OUT_F16);
+    if (ys != DGQ_OK) return ys;
+    p.tma_out = 1;
+  }
+  p.dbg = g_dbg_ts;
+  DGQ_CUDA(dgq_launch_gemm(pl, fused, tmB, tmA, tmY, p, st));
   return DGQ_OK;
 }
 

@@ -44,26 +44,32 @@ struct DgqGemmParams {
   size_t ldy;
   int out_f16;
   int fp16_mode;
+  int vec_ok;  // 16-byte aligned rows: vector epilogue stores allowed
+  int tma_out; // prefill orientation: output written by TMA tensor stores (tmY)
   int32_t* acc_out;  // optional raw int32 accumulators [M x ld_acc]
   size_t ld_acc;
   // split-K workspace (zero on entry, left zero on exit)
   int32_t* ws;
   size_t ldw;
   uint32_t* counters;
+  unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
 };
 
 struct DgqGemmPlan {
   int bn;
+  int nt;  // 128-row weight tiles per CTA
   int m_tiles, n_tiles, splits, kb_per_split;
   size_t smem_bytes;
   size_t ws_bytes;       // split-K accumulator bytes needed (0 if splits == 1)
   size_t counter_bytes;  // split-K tile counters
+  double est_cycles;     // planner's cost-model estimate
+  int pdl;               // launch with programmatic stream serialisation
 };
 
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn = 0, int force_splits = 0);
 
 cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorMap& tmB, const CUtensorMap& tmA,
-                            const DgqGemmParams& p, cudaStream_t st);
+                            const CUtensorMap& tmY, const DgqGemmParams& p, cudaStream_t st);
 
 cudaError_t dgq_launch_actquant(const float* X, size_t ldx, const float* k, int K, int Kpad, int dynamic,
                                 float act_scale, int8_t* Q, size_t ldq, float* rs, int M, cudaStream_t st);
