@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""DGQ A8W4 benchmark (driver contract).
+
+One step = one OPT-30B decoder layer's six DGQ linears at seq M = 2048
+(q, k, v, out 7168x7168; fc1 7168x28672; fc2 28672x7168; g = 128, FP16 out)
+plus the four K1 activation quantisations (one per distinct input: q/k/v
+share theirs).  Weights are column-sharded over the N ranks; the out / fc1 /
+fc2 outputs and the attention stand-in (the q output) are NCCL all-gathered
+and the next K1 reads the gathered [p][M][N/p] buffer in place.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+value = whole-job INT8 TOPS of the step (2*M*sum(K*N) / max-over-ranks time),
+inputs resident in HBM, L2 flushed (256 MiB write) between timed steps.
+e2e   = the same step through the public API with the f32 input copied from
+pinned host memory and the rank's fc2 output shard copied back, every step.
+--impl reference times the reference's own CPU implementation
+(oracle/_ref = /root/reference/proj/src built unmodified) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "A8W4 GEMM TOPS & HBM GB/s (roofline %); OPT-30B layer ms @ seq 512–2048"
+UNIT = "TOPS"
+OPT30B = [("q", 7168, 7168), ("k", 7168, 7168), ("v", 7168, 7168), ("out", 7168, 7168), ("fc1", 7168, 28672),
+          ("fc2", 28672, 7168)]
+GROUP = 128
+SEQ = 2048
+CPU_SAMPLE = dict(name="OPT-30B q_proj", K=7168, N=7168, M=256)
+
+
+def layer_ops(M: int) -> float:
+    return 2.0 * M * sum(k * n for _, k, n in OPT30B)
+
+
+def layer_weight_bytes(world: int = 1) -> float:
+    """Algorithmic HBM bytes of the weights per step per rank (codes + S2 + ZP + s1)."""
+    b = 0.0
+    for _, k, n in OPT30B:
+        ns = n / world
+        b += k * ns / 2 + (k / GROUP) * ns * 1.5 + 4 * ns
+    return b
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and "Active" in r[5 + i] and "Not" not in r[5 + i]:
+                    reasons.add(n)
+        busy = [s for s in sm if mx and s > 0.3 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2310_04836_b200 import synth
+
+    be = oracle.best()
+    K, N, M = CPU_SAMPLE["K"], CPU_SAMPLE["N"], CPU_SAMPLE["M"]
+    L = _oracle_layer(synth.random_layer(K, N, GROUP, seed=7))
+    X = synth.gen_synthetic(M, K, 11, 3, 50.0, 7)
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        be.dgq_forward(X, L, None, 0) if be.kind == "reference" else be.dgq_forward(X, L)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        be.dgq_forward(X, L, None, 0) if be.kind == "reference" else be.dgq_forward(X, L)
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    ops = 2.0 * M * K * N
+    val = ops * len(ts) / tot / 1e12
+    sample = f"{CPU_SAMPLE['name']} ({K}x{N}, g={GROUP}) at M={M} tokens per step, dgq_forward (incl. its per-call weight dequant)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot / len(ts) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int8 (i8 x i8 -> i32, fp32 epilogue)", "data": "synthetic",
+        "config": {"workload": "OPT-30B decoder-layer linears, bounded CPU sample", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": be.kind, "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_layer(L):
+    import oracle
+
+    codes, s2, zp, s1, k = L.arrays()
+    return oracle.Layer(h=L.h, o=L.o, g=L.g, codes=codes, s2=s2, zp=zp, s1=s1, k=k, act_scale=L.act_scale,
+                        mode=L.mode)
+
+
+def cpu_baseline_sample():
+    """Our arm's cpu_baseline: one bounded reference run on the host cores."""
+    import oracle
+    from paper_2310_04836_b200 import synth
+
+    be = oracle.best()
+    K, N, M = CPU_SAMPLE["K"], CPU_SAMPLE["N"], CPU_SAMPLE["M"]
+    L = _oracle_layer(synth.random_layer(K, N, GROUP, seed=7))
+    X = synth.gen_synthetic(M, K, 11, 3, 50.0, 7)
+    t0 = time.perf_counter()
+    be.dgq_forward(X, L, None, 0) if be.kind == "reference" else be.dgq_forward(X, L)
+    t = time.perf_counter() - t0
+    return {"value": 2.0 * M * K * N / t / 1e12, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": be.kind,
+            "sample": f"{CPU_SAMPLE['name']} ({K}x{N}, g={GROUP}) at M={M} tokens, one dgq_forward call "
+                      f"({t:.2f} s, threads = all host cores)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def tiled_layer(K: int, N: int, seed: int, k_vec=None):
+    """A valid random DGQ layer of width N built by tiling a 512-wide random
+    block (values do not affect the data-independent kernels; building 205M
+    random codes on the host per run would dominate the bench)."""
+    import numpy as np
+
+    from paper_2310_04836_b200 import DgqLayer, synth
+
+    base = synth.random_layer(K, 512, GROUP, seed=seed)
+    reps = N // 512
+    codes = np.tile(base.codes.reshape(K, 256), (1, reps))
+    s2 = np.tile(base.s2.reshape(K // GROUP, 512), (1, reps))
+    zp = np.tile(base.zp.reshape(K // GROUP, 256), (1, reps))
+    s1 = np.tile(base.s1, reps)
+    return DgqLayer(h=K, o=N, g=GROUP, codes=codes.ravel(), s2=s2, zp=zp.ravel(), s1=s1,
+                    k=base.k if k_vec is None else k_vec, act_scale=0.0, mode=1)
+
+
+class OptLayer:
+    """The six column-parallel linears of one OPT-30B decoder layer + buffers."""
+
+    def __init__(self, rank, world, device, group, M_max):
+        import torch
+
+        from paper_2310_04836_b200.parallel import ColumnParallelLinear
+
+        self.world, self.device, self.M_max = world, device, M_max
+        qkv_k = None
+        self.lin = {}
+        for i, (name, K, N) in enumerate(OPT30B):
+            L = tiled_layer(K, N, seed=100 + i, k_vec=qkv_k if name in ("k", "v") else None)
+            if name == "q":
+                qkv_k = L.k  # q/k/v share the input and its smoothing vector
+            self.lin[name] = ColumnParallelLinear(L, rank, world, device, group)
+        f16 = torch.float16
+        dev = device
+        self.x = torch.empty(M_max, 7168, dtype=torch.float32, device=dev)
+        self.codes = {n: torch.empty(M_max, self.lin[n].layer.k_pad, dtype=torch.int8, device=dev)
+                      for n in ("q", "out", "fc1", "fc2")}
+        self.rs = {n: torch.empty(M_max, dtype=torch.float32, device=dev) for n in ("q", "out", "fc1", "fc2")}
+        self.y = {n: torch.empty(M_max, self.lin[n].shard, dtype=f16, device=dev) for n, _, _ in OPT30B}
+        self.g = {n: torch.empty(world, M_max, self.lin[n].shard, dtype=f16, device=dev)
+                  for n in ("q", "out", "fc1", "fc2")}
+        self.k_events = []  # (start, end, ops) of the K5 launches while recording
+        self.q_events = []  # (start, end, bytes) of the K1 launches while recording
+        self.record = False
+
+    def _k5(self, name, codes, rs, M):
+        import torch
+
+        lin = self.lin[name]
+        if self.record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+        lin.linear(codes[:M], rs[:M], out=self.y[name][:M])
+        if self.record:
+            b.record()
+            self.k_events.append((a, b, 2.0 * M * lin.h * lin.shard, name))
+
+    def _k1(self, name, x, M):
+        import torch
+
+        lin = self.lin[name]
+        if self.record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+        lin.quantize(x, self.codes[name][:M], self.rs[name][:M])
+        if self.record:
+            b.record()
+            esz = x.element_size()
+            self.q_events.append((a, b, (esz + 1) * M * lin.h + 4 * lin.h + 4 * M, name))
+
+    def _gather(self, name, M):
+        lin = self.lin[name]
+        if self.world == 1:
+            return self.y[name][:M].unsqueeze(0)
+        out = self.g[name][:, :M]
+        if M == self.M_max:
+            lin.gather(self.y[name], out=self.g[name])
+            return self.g[name]
+        import torch.distributed as dist
+
+        buf = self.g[name].view(-1)[: self.world * M * lin.shard].view(self.world, M, lin.shard)
+        dist.all_gather_into_tensor(buf.view(self.world * M, lin.shard), self.y[name][:M].contiguous(),
+                                    group=lin.group)
+        return buf
+
+    def step(self, M):
+        """One decoder layer's linears for M tokens; returns this rank's fc2 shard."""
+        x = self.x[:M]
+        self._k1("q", x, M)
+        cq, rq = self.codes["q"], self.rs["q"]
+        for n in ("q", "k", "v"):
+            self._k5(n, cq, rq, M)
+        a = self._gather("q", M)  # attention-output stand-in, gathered for the out projection
+        self._k1("out", a, M)
+        self._k5("out", self.codes["out"], self.rs["out"], M)
+        go = self._gather("out", M)
+        self._k1("fc1", go, M)
+        self._k5("fc1", self.codes["fc1"], self.rs["fc1"], M)
+        g1 = self._gather("fc1", M)
+        self._k1("fc2", g1, M)
+        self._k5("fc2", self.codes["fc2"], self.rs["fc2"], M)
+        self._gather("fc2", M)
+        return self.y["fc2"][:M]
+
+
+def timed_steps(layer, M, steps, warmup, flush, sync_all, e2e=None):
+    """Per-step CUDA-event times (s) with an L2 flush between steps; with e2e =
+    (x_host, out_host) the step includes the H2D input copy and D2H output copy."""
+    import torch
+
+    def one():
+        if e2e is not None:
+            layer.x[:M].copy_(e2e[0], non_blocking=True)
+        y = layer.step(M)
+        if e2e is not None:
+            e2e[1].copy_(y, non_blocking=True)
+
+    for _ in range(warmup):
+        one()
+    sync_all()
+    times = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        one()
+        b.record()
+        b.synchronize()
+        times.append(a.elapsed_time(b) * 1e-3)
+    sync_all()
+    return times
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    import paper_2310_04836_b200 as dgq
+
+    dgq.lib()
+    hbm_peak, bf16_peak, peak_src = load_peaks()
+    i8_peak = 2.0 * bf16_peak  # proxy: dense INT8 = 2x dense BF16 (FP8-class rate); spec 4500
+    layer = OptLayer(rank, world, device, group, SEQ)
+    torch.manual_seed(1234 + 0)
+    x_host = (torch.randn(SEQ, 7168) * 2.0).pin_memory()
+    x_host[:, 17] *= 50  # outlier channels, as the reference's synthetic activations
+    x_host[:, 4001] *= 50
+    layer.x.copy_(x_host)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    sync_all()
+
+    # ---- headline: device-resident step at seq 2048 ------------------------------------------
+    clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    layer.record = False
+    for _ in range(args.warmup):
+        layer.step(SEQ)
+    sync_all()
+    clocks.start()
+    layer.record = True
+    times = timed_steps(layer, SEQ, args.steps, 0, flush, sync_all)
+    layer.record = False
+    clk = clocks.stop()
+    total = max_over_ranks(sum(times))
+    ops_step = layer_ops(SEQ)
+    value = ops_step * args.steps / total / 1e12
+    ms_per_step = total / args.steps * 1e3
+
+    # roofline of the dominant kernel (K5), measured over the timed region
+    k5_t = sum(a.elapsed_time(b) * 1e-3 for a, b, _, _ in layer.k_events)
+    k5_ops = sum(o for _, _, o, _ in layer.k_events)
+    k5_tops = k5_ops / k5_t / 1e12
+    by_name = {}
+    for a, b, o, n in layer.k_events:
+        t, oo = by_name.get(n, (0.0, 0.0))
+        by_name[n] = (t + a.elapsed_time(b) * 1e-3, oo + o)
+    k1_t = sum(a.elapsed_time(b) * 1e-3 for a, b, _, _ in layer.q_events)
+    k1_b = sum(bb for _, _, bb, _ in layer.q_events)
+    n_launches = len(layer.k_events) + len(layer.q_events)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("k5_fc1_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API with host buffers ---------------------------------------
+    out_host = torch.empty(SEQ, layer.lin["fc2"].shard, dtype=torch.float16).pin_memory()
+    e2e_times = timed_steps(layer, SEQ, args.steps, 1, flush, sync_all, e2e=(x_host, out_host))
+    e2e_total = max_over_ranks(sum(e2e_times))
+    e2e_val = ops_step * args.steps / e2e_total / 1e12
+
+    # ---- detail: layer ms at seq 512 / 1024, decode (M = 16) weight bandwidth ----------------
+    detail = {}
+    if not args.no_detail:
+        for M in (512, 1024):
+            t = timed_steps(layer, M, 3, 1, flush, sync_all)
+            tm = max_over_ranks(sum(t)) / 3
+            detail[f"layer_ms_seq{M}"] = tm * 1e3
+            detail[f"tops_seq{M}"] = layer_ops(M) / tm / 1e12
+        detail["layer_ms_seq2048"] = ms_per_step
+        for M in (1, 16):
+            t = timed_steps(layer, M, 5, 2, flush, sync_all)
+            tm = max_over_ranks(sum(t)) / 5
+            wb = layer_weight_bytes(world)
+            detail[f"decode_m{M}_layer_us"] = tm * 1e6
+            detail[f"decode_m{M}_weight_GBps_per_gpu"] = wb / tm / 1e9
+            detail[f"decode_m{M}_hbm_frac"] = wb / tm / 1e9 / hbm_peak
+        detail["k5_tops_by_linear"] = {n: o / t / 1e12 for n, (t, o) in by_name.items()}
+        detail["k1_GBps"] = k1_b / k1_t / 1e9
+        plans = {n: layer.lin[n].layer.plan(SEQ) for n in ("q", "fc1", "fc2")}
+        detail["plans_seq2048"] = plans
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_sample()
+        except Exception as e:  # oracle not built on this box
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable", "sample": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int8 (i8 x i8 -> i32 tcgen05 kind::i8; fp32 scales; fp16 out)",
+            "data": "synthetic (random valid DGQ layers, Gaussian activations with outlier channels)",
+            "config": {
+                "workload": "OPT-30B decoder-layer linears (q,k,v,out 7168x7168; fc1 7168x28672; fc2 28672x7168) "
+                            "+ 4 activation quantisations, seq 2048, g=128, FP16 out",
+                "seq_len": SEQ, "group": GROUP, "parallelism": f"column-parallel N-shard x{world} (NCCL all-gather)",
+                "l2": "flushed between timed steps (256 MiB write); per-GPU weights "
+                      f"{layer_weight_bytes(world) / 1e6:.0f} MB",
+            },
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": SEQ * 7168 * 4,
+                    "d2h_bytes_per_step": SEQ * layer.lin["fc2"].shard * 2, "per": "rank"},
+            "gpu_launches": n_launches,
+            "roofline": {"bound": "tensor", "kernel": "K5 fused DGQ linear (all six launches per step)",
+                         "achieved": k5_tops, "peak": i8_peak, "unit": "TFLOP/s", "frac": k5_tops / i8_peak,
+                         "peak_note": f"dense INT8 proxy = 2 x bf16 burst {bf16_peak} TF/s, {peak_src}; "
+                                      f"NVIDIA spec dense INT8 4500 TOPS -> frac {k5_tops / 4500:.3f}",
+                         "traffic": traffic},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "detail": detail,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-detail", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

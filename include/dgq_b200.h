@@ -109,6 +109,12 @@ dgq_status dgq_linear_plan(const dgq_layer* layer, size_t M, int* token_tile, in
  * are zero-filled. */
 dgq_status dgq_quantize_act(const dgq_layer* layer, const float* dX, size_t M, size_t ldx, int8_t* dXq, size_t ldq,
                             float* dRowScale, void* stream);
+/* FP16 activations (the inter-layer format; float(x_f16) is exact, so the codes
+ * equal dgq_quantize_act on the float32 copy).  seg_cols > 0 reads the
+ * all-gather of column shards: element (m, j) at
+ * dX[(j / seg_cols) * seg_stride + m * ldx + j % seg_cols]. */
+dgq_status dgq_quantize_act_f16(const dgq_layer* layer, const void* dX, size_t M, size_t ldx, size_t seg_cols,
+                                size_t seg_stride, int8_t* dXq, size_t ldq, float* dRowScale, void* stream);
 dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx, const float* dK, int mode,
                                 float act_scale, int8_t* dXq, size_t ldq, float* dRowScale, void* stream);
 

@@ -70,6 +70,7 @@ _SIGS = {
     "dgq_linear_workspace_bytes": (_sz, [_vp, _sz]),
     "dgq_linear_plan": (_i, [_vp, _sz, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "dgq_quantize_act": (_i, [_vp, _vp, _sz, _sz, _vp, _sz, _vp, _vp]),
+    "dgq_quantize_act_f16": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _sz, _vp, _vp]),
     "dgq_quantize_act_raw": (_i, [_vp, _sz, _sz, _sz, _vp, _i, _f, _vp, _sz, _vp, _vp]),
     "dgq_linear": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _i, _vp, _sz, _vp, _sz, _vp, _sz, _vp]),
     "dgq_forward_device": (_i, [_vp, _vp, _sz, _sz, _vp, _i, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),

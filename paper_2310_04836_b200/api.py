@@ -206,16 +206,29 @@ class CudaLayer:
 
     # K1
     def quantize_act(self, x: torch.Tensor, codes: torch.Tensor | None = None, rs: torch.Tensor | None = None):
-        """x: cuda float32 [M, h] -> (codes int8 [M, k_pad] zero padded, row_scales float32 [M])."""
-        assert x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 and x.shape[1] == self.h
-        assert x.stride(1) == 1
-        M = x.shape[0]
+        """x: cuda float32 or float16 [M, h] -> (codes int8 [M, k_pad] zero padded, row_scales float32 [M]).
+        A float16 x may also be an all-gathered [p, M, h/p] shard stack (read in place)."""
+        assert x.is_cuda and x.dtype in (torch.float32, torch.float16)
+        gathered = x.dim() == 3
+        if gathered:
+            p_, M, seg = x.shape
+            assert x.dtype == torch.float16 and p_ * seg == self.h and x.stride(2) == 1
+        else:
+            assert x.dim() == 2 and x.shape[1] == self.h and x.stride(1) == 1
+            M = x.shape[0]
         if codes is None:
             codes = torch.empty(M, self.k_pad, dtype=torch.int8, device=x.device)
         if rs is None:
             rs = torch.empty(M, dtype=torch.float32, device=x.device)
-        check(lib().dgq_quantize_act(self._h, _t_ptr(x), M, x.stride(0), _t_ptr(codes), codes.stride(0),
-                                     _t_ptr(rs), _stream(x.device)))
+        if x.dtype == torch.float32:
+            check(lib().dgq_quantize_act(self._h, _t_ptr(x), M, x.stride(0), _t_ptr(codes), codes.stride(0),
+                                         _t_ptr(rs), _stream(x.device)))
+        elif gathered:
+            check(lib().dgq_quantize_act_f16(self._h, _t_ptr(x), M, x.stride(1), seg, x.stride(0), _t_ptr(codes),
+                                             codes.stride(0), _t_ptr(rs), _stream(x.device)))
+        else:
+            check(lib().dgq_quantize_act_f16(self._h, _t_ptr(x), M, x.stride(0), 0, 0, _t_ptr(codes),
+                                             codes.stride(0), _t_ptr(rs), _stream(x.device)))
         return codes, rs
 
     # K5

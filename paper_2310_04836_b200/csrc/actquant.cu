@@ -10,10 +10,17 @@
 // padded stride ldq >= K and the pad columns zero-filled, which is the
 // layout the GEMM's TMA expects.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
+
+#include <cooperative_groups.h>
+#include <cuda_fp16.h>
 
 #include "kernels.h"
 #include "numerics.cuh"
+#include "ptx.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dgqk {
 
@@ -125,6 +132,319 @@ __global__ void __launch_bounds__(T) k_actquant_any(const float* __restrict__ X,
   }
 }
 
+// FP16 input (the inter-layer activation format), optionally stored as the
+// all-gather of column shards: logical element (m, j) lives at
+//   X + (j / seg) * seg_stride + m * ldx + (j % seg)
+// so the next layer quantises the gathered [p][M][K/p] buffer in place.
+// float(x_f16) is exact, so this equals K1 on the float32 copy bit-for-bit.
+template <int T, int V>
+__global__ void __launch_bounds__(T) k_actquant_h8(const __half* __restrict__ X, size_t ldx, int seg, size_t seg_stride,
+                                                    const float* __restrict__ kv, int K, int Kpad, int dynamic,
+                                                    float act_scale, int8_t* __restrict__ Q, size_t ldq,
+                                                    float* __restrict__ rs, int M) {
+  __shared__ float red[33];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int K8 = K >> 3;
+  for (int row = blockIdx.x; row < M; row += gridDim.x) {
+    float xv[V][8];
+    float am = 0.0f;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int i = threadIdx.x + v * T;
+      if (i < K8) {
+        const int j = i * 8;
+        const __half* src = X + static_cast<size_t>(j / seg) * seg_stride + static_cast<size_t>(row) * ldx + (j % seg);
+        const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(src));
+        const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
+        const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
+        const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+        const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 f = __half22float2(h2[t]);
+          xv[v][2 * t] = __fdiv_rn(f.x, kk[2 * t]);
+          xv[v][2 * t + 1] = __fdiv_rn(f.y, kk[2 * t + 1]);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
+      }
+    }
+    float s = act_scale;
+    if (dynamic) s = dynamic_row_scale(block_max<T>(am, red));
+    if (threadIdx.x == 0) rs[row] = s;
+    uint2* qr = reinterpret_cast<uint2*>(Q + static_cast<size_t>(row) * ldq);
+    const bool safe = scale_is_safe(s);
+    const float inv = __frcp_rn(s);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int i = threadIdx.x + v * T;
+      if (i < K8) {
+        int c[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) c[t] = safe ? quant_code_f32(xv[v][t], s, inv) : quant_code_f64(xv[v][t], s);
+        qr[i] = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
+      }
+    }
+    for (int i = K8 + threadIdx.x; i < (Kpad >> 3); i += T) qr[i] = make_uint2(0u, 0u);
+  }
+}
+
+// Generic FP16 path (any K / segment geometry).
+template <int T>
+__global__ void __launch_bounds__(T) k_actquant_h_any(const __half* __restrict__ X, size_t ldx, int seg,
+                                                       size_t seg_stride, const float* __restrict__ kv, int K,
+                                                       int Kpad, int dynamic, float act_scale,
+                                                       int8_t* __restrict__ Q, size_t ldq, float* __restrict__ rs,
+                                                       int M) {
+  __shared__ float red[33];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int row = blockIdx.x; row < M; row += gridDim.x) {
+    auto at = [&](int j) {
+      return __half2float(X[static_cast<size_t>(j / seg) * seg_stride + static_cast<size_t>(row) * ldx + (j % seg)]);
+    };
+    float s = act_scale;
+    if (dynamic) {
+      float am = 0.0f;
+      for (int j = threadIdx.x; j < K; j += T) am = fmaxf(am, fabsf(__fdiv_rn(at(j), kv[j])));
+      s = dynamic_row_scale(block_max<T>(am, red));
+    }
+    if (threadIdx.x == 0) rs[row] = s;
+    int8_t* qr = Q + static_cast<size_t>(row) * ldq;
+    const bool safe = scale_is_safe(s);
+    const float inv = __frcp_rn(s);
+    for (int j = threadIdx.x; j < K; j += T) {
+      const float x = __fdiv_rn(at(j), kv[j]);
+      qr[j] = static_cast<int8_t>(safe ? quant_code_f32(x, s, inv) : quant_code_f64(x, s));
+    }
+    for (int j = K + threadIdx.x; j < Kpad; j += T) qr[j] = 0;
+  }
+}
+
+// ---- K1 v2: one row per CL-CTA cluster, 8-element chunks, loads front-loaded ----
+// chunk c of a row (elements 8c..8c+7) belongs to cluster rank c / (T*V); every
+// thread first issues all of its V 16-B (f16) or 32-B (f32) loads, then divides
+// by k with the hoisted reciprocal (div_k), reduces the row absmax (block, then
+// over the cluster through DSMEM), and quantises from registers.
+template <int T, int V, int CL, bool kF16, bool kCheckK>
+__global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
+                                                  const float* __restrict__ kv, const float* __restrict__ rkv, int K,
+                                                  int Kpad, int dynamic, float act_scale, int8_t* __restrict__ Q,
+                                                  size_t ldq, float* __restrict__ rs, int M) {
+  __shared__ float red[33];
+  __shared__ float cl_max;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int row = blockIdx.x / CL;
+  const int part = blockIdx.x % CL;
+  if (row >= M) return;  // grid is exactly M*CL; keeps the cluster barrier uniform
+  const int C8 = K >> 3;
+  const int cbase = part * T * V + threadIdx.x;
+  uint4 raw[V][kF16 ? 1 : 2];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c = cbase + v * T;
+    if (c < C8) {
+      const int j = c * 8;
+      if constexpr (kF16) {
+        const __half* src = static_cast<const __half*>(Xv) + static_cast<size_t>(j / seg) * seg_stride +
+                            static_cast<size_t>(row) * ldx + (j % seg);
+        raw[v][0] = __ldcs(reinterpret_cast<const uint4*>(src));
+      } else {
+        const float* src = static_cast<const float*>(Xv) + static_cast<size_t>(row) * ldx + j;
+        raw[v][0] = __ldcs(reinterpret_cast<const uint4*>(src));
+        raw[v][1] = __ldcs(reinterpret_cast<const uint4*>(src + 4));
+      }
+    }
+  }
+  float xv[V][8];
+  float am = 0.0f;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c = cbase + v * T;
+    if (c < C8) {
+      const int j = c * 8;
+      const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
+      const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
+      const float4 r0 = __ldg(reinterpret_cast<const float4*>(rkv + j));
+      const float4 r1 = __ldg(reinterpret_cast<const float4*>(rkv + j + 4));
+      const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+      const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      float x[8];
+      if constexpr (kF16) {
+        const __half2* h2 = reinterpret_cast<const __half2*>(&raw[v][0]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 f = __half22float2(h2[t]);
+          x[2 * t] = f.x;
+          x[2 * t + 1] = f.y;
+        }
+      } else {
+        const float* f = reinterpret_cast<const float*>(&raw[v][0]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[t] = f[t];
+      }
+      div_chunk<!kF16, kCheckK>(x, kk, rr, xv[v]);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
+    }
+  }
+  float s = act_scale;
+  if (dynamic) {
+    float bm = block_max<T>(am, red);
+    if constexpr (CL > 1) {
+      cg::cluster_group cluster = cg::this_cluster();
+      if (threadIdx.x == 0) cl_max = bm;
+      cluster.sync();
+#pragma unroll
+      for (int r = 0; r < CL; ++r) bm = fmaxf(bm, *cluster.map_shared_rank(&cl_max, r));
+      cluster.sync();  // peers finished reading cl_max
+    }
+    s = dynamic_row_scale(bm);
+  }
+  if (part == 0 && threadIdx.x == 0) rs[row] = s;
+  uint2* qr = reinterpret_cast<uint2*>(Q + static_cast<size_t>(row) * ldq);
+  const bool safe = scale_is_safe(s);
+  const float inv = __frcp_rn(s);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c = cbase + v * T;
+    if (c < C8) {
+      int o[8];
+      if (safe) {
+        quant_chunk(xv[v], s, inv, o);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) o[t] = quant_code_f64(xv[v][t], s);
+      }
+      qr[c] = make_uint2(pack4(o[0], o[1], o[2], o[3]), pack4(o[4], o[5], o[6], o[7]));
+    }
+  }
+  if (part == 0)
+    for (int c = C8 + threadIdx.x; c < (Kpad >> 3); c += T) qr[c] = make_uint2(0u, 0u);
+}
+
+// ---- K1 v3 (large M): persistent CTAs, whole rows staged in shared memory by
+// 1-D TMA bulk copies two rows ahead (double buffer, one mbarrier each), so
+// the HBM stream never waits for the divide / reduce / quantise of the
+// previous row.  x' = x/k stays in registers between the absmax and the codes.
+template <int T, int V, bool kF16, bool kCheckK>
+__global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
+                                                  const float* __restrict__ kv, const float* __restrict__ rkv, int K,
+                                                  int Kpad, int dynamic, float act_scale, int8_t* __restrict__ Q,
+                                                  size_t ldq, float* __restrict__ rs, int M) {
+  extern __shared__ __align__(128) uint8_t sbuf[];
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ float red[33];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int kEsz = kF16 ? 2 : 4;
+  const uint32_t rowbytes = static_cast<uint32_t>(K) * kEsz;
+  const uint32_t bufstride = (rowbytes + 127u) & ~127u;
+  const int C8 = K >> 3;
+  const int nseg = K / seg;
+  auto issue = [&](int r, int b) {  // thread 0 only
+    dgqk::mbar_arrive_expect_tx(&full[b], rowbytes);
+    for (int sg = 0; sg < nseg; ++sg) {
+      const uint8_t* src = static_cast<const uint8_t*>(Xv) +
+                           (static_cast<size_t>(sg) * seg_stride + static_cast<size_t>(r) * ldx) * kEsz;
+      dgqk::bulk_load(sbuf + b * bufstride + static_cast<size_t>(sg) * seg * kEsz, src,
+                      static_cast<uint32_t>(seg) * kEsz, &full[b]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    dgqk::mbar_init(&full[0], 1);
+    dgqk::mbar_init(&full[1], 1);
+    dgqk::fence_mbar_init();
+  }
+  __syncthreads();
+  int it = 0;
+  if (threadIdx.x == 0) {
+    if (static_cast<int>(blockIdx.x) < M) issue(blockIdx.x, 0);
+    if (static_cast<int>(blockIdx.x + gridDim.x) < M) issue(blockIdx.x + gridDim.x, 1);
+  }
+  for (int row = blockIdx.x; row < M; row += gridDim.x, ++it) {
+    const int b = it & 1;
+    dgqk::mbar_wait(&full[b], (it >> 1) & 1);
+    const uint8_t* buf = sbuf + b * bufstride;
+    float xv[V][8];
+    float am = 0.0f;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = threadIdx.x + v * T;
+      if (c < C8) {
+        const int j = c * 8;
+        float x[8];
+        if constexpr (kF16) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(buf + j * 2);
+          const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 f = __half22float2(h2[t]);
+            x[2 * t] = f.x;
+            x[2 * t + 1] = f.y;
+          }
+        } else {
+          const float4 a = *reinterpret_cast<const float4*>(buf + j * 4);
+          const float4 bb = *reinterpret_cast<const float4*>(buf + j * 4 + 16);
+          x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+          x[4] = bb.x; x[5] = bb.y; x[6] = bb.z; x[7] = bb.w;
+        }
+        const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
+        const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
+        const float4 r0 = __ldg(reinterpret_cast<const float4*>(rkv + j));
+        const float4 r1 = __ldg(reinterpret_cast<const float4*>(rkv + j + 4));
+        const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+        const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        div_chunk<!kF16, kCheckK>(x, kk, rr, xv[v]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
+      }
+    }
+    float s = act_scale;
+    if (dynamic) {
+      s = dynamic_row_scale(block_max<T>(am, red));  // its barriers also retire every read of buf
+    } else {
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      rs[row] = s;
+      const int nxt = row + 2 * gridDim.x;
+      if (nxt < M) issue(nxt, b);
+    }
+    uint2* qr = reinterpret_cast<uint2*>(Q + static_cast<size_t>(row) * ldq);
+    const bool safe = scale_is_safe(s);
+    const float inv = __frcp_rn(s);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int c = threadIdx.x + v * T;
+      if (c < C8) {
+        int o[8];
+        if (safe) {
+          quant_chunk(xv[v], s, inv, o);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) o[t] = quant_code_f64(xv[v][t], s);
+        }
+        qr[c] = make_uint2(pack4(o[0], o[1], o[2], o[3]), pack4(o[4], o[5], o[6], o[7]));
+      }
+    }
+    for (int c = C8 + threadIdx.x; c < (Kpad >> 3); c += T) qr[c] = make_uint2(0u, 0u);
+  }
+}
+
+__global__ void k_reciprocal(const float* __restrict__ k, float* __restrict__ rk, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rk[i] = (k[i] <= 0x1p24f) ? __frcp_rn(k[i]) : 0.0f;  // 0 marks k outside div_k's fast range
+}
+
+// unit test hook: y[i] = div_k(x[i], k[i], RN(1/k[i])) next to __fdiv_rn
+__global__ void k_div_check(const float* __restrict__ x, const float* __restrict__ k, float* __restrict__ fast,
+                            float* __restrict__ ieee, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    fast[i] = div_k(x[i], k[i], __frcp_rn(k[i]));
+    ieee[i] = __fdiv_rn(x[i], k[i]);
+  }
+}
+
 }  // namespace dgqk
 
 using namespace dgqk;
@@ -152,5 +472,137 @@ cudaError_t dgq_launch_actquant(const float* X, size_t ldx, const float* k, int 
   } else {
     k_actquant_any<256><<<grid, 256, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t dgq_launch_actquant_f16(const void* Xv, size_t ldx, int seg, size_t seg_stride, const float* k, int K,
+                                    int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq, float* rs, int M,
+                                    cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  const __half* X = static_cast<const __half*>(Xv);
+  if (seg <= 0) seg = K;
+  const bool vec = (K % 8 == 0) && (seg % 8 == 0) && (ldx % 8 == 0) && (seg_stride % 8 == 0) && (ldq % 8 == 0) &&
+                   (Kpad % 8 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(k) % 16 == 0) && (reinterpret_cast<uintptr_t>(Q) % 8 == 0);
+  const int K8 = K / 8;
+#define DGQ_H8(T_, V_) k_actquant_h8<T_, V_><<<M, T_, 0, st>>>(X, ldx, seg, seg_stride, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M)
+  if (vec && K8 <= 128) DGQ_H8(128, 1);
+  else if (vec && K8 <= 256) DGQ_H8(256, 1);
+  else if (vec && K8 <= 512) DGQ_H8(256, 2);
+  else if (vec && K8 <= 1024) DGQ_H8(256, 4);
+  else if (vec && K8 <= 2048) DGQ_H8(512, 4);
+  else if (vec && K8 <= 4096) DGQ_H8(512, 8);
+  else k_actquant_h_any<256><<<M, 256, 0, st>>>(X, ldx, seg, seg_stride, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
+#undef DGQ_H8
+  return cudaGetLastError();
+}
+
+namespace {
+template <int T, int V, int CL, bool F16, bool CK>
+cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, const float* rk, int K,
+                       int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq, float* rs, int M,
+                       cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(M) * CL);
+  cfg.blockDim = dim3(T);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CL > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, CK>, X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,
+                            act_scale, Q, ldq, rs, M);
+}
+}  // namespace
+
+cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, size_t seg_stride, const float* k,
+                                 const float* rk, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
+                                 float* rs, int M, cudaStream_t st, bool k_checked) {
+  if (M <= 0) return cudaSuccess;
+  if (seg <= 0) seg = K;
+  const size_t align = f16 ? 8 : 4;  // elements per 16 bytes
+  const bool vec = rk && (K % 8 == 0) && (seg % 8 == 0) && (ldx % align == 0) && (seg_stride % align == 0) &&
+                   (ldq % 8 == 0) && (Kpad % 8 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(k) % 16 == 0) && (reinterpret_cast<uintptr_t>(rk) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(Q) % 8 == 0) && (f16 || seg == K);
+  if (!vec) {
+    if (f16)
+      k_actquant_h_any<256><<<M, 256, 0, st>>>(static_cast<const __half*>(X), ldx, seg, seg_stride, k, K, Kpad,
+                                                dynamic, act_scale, Q, ldq, rs, M);
+    else
+      k_actquant_any<256><<<M, 256, 0, st>>>(static_cast<const float*>(X), ldx, k, K, Kpad, dynamic, act_scale, Q,
+                                              ldq, rs, M);
+    return cudaGetLastError();
+  }
+  const int C8 = K / 8;
+  cudaError_t e;
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t stage = 2 * ((static_cast<size_t>(K) * (f16 ? 2 : 4) + 127) & ~size_t(127));
+  if (M >= n_sm && C8 <= 4096 && stage <= 220 * 1024) {
+#define DGQ_AQ3(T_, V_)                                                                                         \
+  {                                                                                                             \
+    auto kern = f16 ? (k_checked ? k_actquant3<T_, V_, true, false> : k_actquant3<T_, V_, true, true>)          \
+                    : (k_checked ? k_actquant3<T_, V_, false, false> : k_actquant3<T_, V_, false, true>);       \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(stage));          \
+    int occ = 1;                                                                                                \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, stage);                                       \
+    const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \
+    kern<<<grid, T_, stage, st>>>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);  \
+    return cudaGetLastError();                                                                                  \
+  }
+    if (C8 <= 256) DGQ_AQ3(256, 1)
+    if (C8 <= 512) DGQ_AQ3(256, 2)
+    if (C8 <= 1024) DGQ_AQ3(256, 4)
+    if (C8 <= 2048) DGQ_AQ3(512, 4)
+    DGQ_AQ3(512, 8)
+#undef DGQ_AQ3
+  }
+#define DGQ_AQ(T_, V_, CL_)                                                                                    \
+  e = f16 ? (k_checked ? launch_aq2<T_, V_, CL_, true, false>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,    \
+                                                               act_scale, Q, ldq, rs, M, st)                     \
+                       : launch_aq2<T_, V_, CL_, true, true>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,     \
+                                                              act_scale, Q, ldq, rs, M, st))                     \
+          : (k_checked ? launch_aq2<T_, V_, CL_, false, false>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,   \
+                                                                act_scale, Q, ldq, rs, M, st)                    \
+                       : launch_aq2<T_, V_, CL_, false, true>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,    \
+                                                               act_scale, Q, ldq, rs, M, st))
+  if (C8 <= 128) DGQ_AQ(128, 1, 1);
+  else if (C8 <= 256) DGQ_AQ(128, 2, 1);
+  else if (C8 <= 512) DGQ_AQ(128, 4, 1);
+  else if (C8 <= 1024) DGQ_AQ(256, 4, 1);
+  else if (C8 <= 2048) DGQ_AQ(256, 4, 2);
+  else if (C8 <= 4096) DGQ_AQ(256, 4, 4);
+  else if (C8 <= 8192) DGQ_AQ(256, 4, 8);
+  else {
+    if (f16)
+      k_actquant_h_any<256><<<M, 256, 0, st>>>(static_cast<const __half*>(X), ldx, seg, seg_stride, k, K, Kpad,
+                                                dynamic, act_scale, Q, ldq, rs, M);
+    else
+      k_actquant_any<256><<<M, 256, 0, st>>>(static_cast<const float*>(X), ldx, k, K, Kpad, dynamic, act_scale, Q,
+                                              ldq, rs, M);
+    e = cudaSuccess;
+  }
+#undef DGQ_AQ
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t dgq_launch_reciprocal(const float* k, float* rk, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_reciprocal<<<(n + 255) / 256, 256, 0, st>>>(k, rk, n);
+  return cudaGetLastError();
+}
+
+cudaError_t dgq_launch_div_check(const float* x, const float* k, float* fast, float* ieee, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_div_check<<<(n + 255) / 256, 256, 0, st>>>(x, k, fast, ieee, n);
   return cudaGetLastError();
 }

@@ -103,6 +103,8 @@ struct dgq_layer {
   int8_t* wt = nullptr;      // non-fused: W_s8^T [n_pad x k_pad]
   float* s1 = nullptr;       // [o] (this shard)
   float* k = nullptr;        // [h]
+  float* rk = nullptr;       // [h] RN(1/k): hoisted reciprocals for K1
+  bool k_fast = false;       // every k <= 2^24: K1 skips the per-chunk k range check
   size_t device_bytes = 0;
   CUtensorMap tmA{};  // non-fused A operand
   std::mutex ws_mu;
@@ -217,6 +219,7 @@ void dgq_layer_destroy(dgq_layer* L) {
   cudaFree(L->wt);
   cudaFree(L->s1);
   cudaFree(L->k);
+  cudaFree(L->rk);
   cudaFree(L->ws);
   cudaSetDevice(prev);
   delete L;
@@ -284,6 +287,10 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
   DGQ_CUDA_L(cudaMalloc(&L->k, h * sizeof(float)));
   DGQ_CUDA_L(cudaMemcpyAsync(L->s1, s1 + col_begin, L->o * sizeof(float), cudaMemcpyHostToDevice, st));
   DGQ_CUDA_L(cudaMemcpyAsync(L->k, k, h * sizeof(float), cudaMemcpyHostToDevice, st));
+  DGQ_CUDA_L(cudaMalloc(&L->rk, h * sizeof(float)));
+  L->k_fast = true;
+  for (size_t j = 0; j < h; ++j) L->k_fast = L->k_fast && k[j] <= 0x1p24f;
+  DGQ_CUDA_L(dgq_launch_reciprocal(L->k, L->rk, static_cast<int>(h), st));
   L->device_bytes = (L->o + h) * sizeof(float);
   if (L->fused) {
     const size_t tb = static_cast<size_t>(L->n_tiles) * L->k_blocks * dgq_layout::chunk_bytes(static_cast<int>(g));
@@ -409,15 +416,50 @@ dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx,
   if (!dX || !dK || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
   if (ldx < K || ldq < K) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
   if (M > 0x7FFFFFFF || K > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too large");
-  DGQ_CUDA(dgq_launch_actquant(dX, ldx, dK, static_cast<int>(K), static_cast<int>(ldq), mode != 0, act_scale, dXq,
-                               ldq, dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream)));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* rk = nullptr;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rk), (K ? K : 1) * sizeof(float), st));
+  DGQ_CUDA(dgq_launch_reciprocal(dK, rk, static_cast<int>(K), st));
+  cudaError_t e = dgq_launch_actquant2(dX, false, ldx, static_cast<int>(K), 0, dK, rk, static_cast<int>(K),
+                                       static_cast<int>(ldq), mode != 0, act_scale, dXq, ldq, dRowScale,
+                                       static_cast<int>(M), st);
+  cudaFreeAsync(rk, st);
+  DGQ_CUDA(e);
+  return DGQ_OK;
+}
+
+/* not in the public header: test hook pinning the hoisted-reciprocal division to IEEE div.rn */
+dgq_status dgq_debug_div_check(const float* dx, const float* dk, float* dfast, float* dieee, size_t n, void* stream) {
+  DGQ_CUDA(dgq_launch_div_check(dx, dk, dfast, dieee, static_cast<int>(n), static_cast<cudaStream_t>(stream)));
+  return DGQ_OK;
+}
+
+dgq_status dgq_quantize_act_f16(const dgq_layer* L, const void* dX, size_t M, size_t ldx, size_t seg_cols,
+                                size_t seg_stride, int8_t* dXq, size_t ldq, float* dRowScale, void* stream) {
+  if (!L) return fail(DGQ_EINVAL, "null layer");
+  if (M == 0) return DGQ_OK;
+  if (!dX || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
+  const size_t seg = seg_cols ? seg_cols : L->h;
+  if (L->h % seg) return fail(DGQ_EINVAL, "seg_cols must divide h");
+  if (ldx < seg || ldq < L->h) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
+  if (seg_cols && seg_stride < M * ldx) return fail(DGQ_EINVAL, "seg_stride smaller than one shard");
+  DGQ_CUDA(dgq_launch_actquant2(dX, true, ldx, static_cast<int>(seg), seg_stride, L->k, L->rk,
+                                static_cast<int>(L->h), static_cast<int>(ldq), L->mode, L->act_scale, dXq, ldq,
+                                dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast));
   return DGQ_OK;
 }
 
 dgq_status dgq_quantize_act(const dgq_layer* L, const float* dX, size_t M, size_t ldx, int8_t* dXq, size_t ldq,
                             float* dRowScale, void* stream) {
   if (!L) return fail(DGQ_EINVAL, "null layer");
-  return dgq_quantize_act_raw(dX, M, L->h, ldx, L->k, L->mode, L->act_scale, dXq, ldq, dRowScale, stream);
+  if (M == 0) return DGQ_OK;
+  if (!dX || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
+  if (ldx < L->h || ldq < L->h) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
+  if (M > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too many rows");
+  DGQ_CUDA(dgq_launch_actquant2(dX, false, ldx, static_cast<int>(L->h), 0, L->k, L->rk, static_cast<int>(L->h),
+                                static_cast<int>(ldq), L->mode, L->act_scale, dXq, ldq, dRowScale,
+                                static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast));
+  return DGQ_OK;
 }
 
 static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& tmA, int g, size_t N, size_t k_pad,

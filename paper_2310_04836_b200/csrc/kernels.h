@@ -74,6 +74,19 @@ cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorM
 cudaError_t dgq_launch_actquant(const float* X, size_t ldx, const float* k, int K, int Kpad, int dynamic,
                                 float act_scale, int8_t* Q, size_t ldq, float* rs, int M, cudaStream_t st);
 
+// K1 v2 (f32 or f16 input; f16 may be the all-gathered [p][M][seg] layout);
+// rk = RN(1/k) per input channel (dgq_launch_reciprocal).
+cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, size_t seg_stride, const float* k,
+                                 const float* rk, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
+                                 float* rs, int M, cudaStream_t st, bool k_checked = false);
+cudaError_t dgq_launch_reciprocal(const float* k, float* rk, int n, cudaStream_t st);
+cudaError_t dgq_launch_div_check(const float* x, const float* k, float* fast, float* ieee, int n, cudaStream_t st);
+
+// FP16 activations, optionally the all-gathered [p][M][seg] layout (seg = K/p).
+cudaError_t dgq_launch_actquant_f16(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, int K,
+                                    int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq, float* rs, int M,
+                                    cudaStream_t st);
+
 // Reference layout (codes u4 [h x o_full] packed along o, s2 i8, zp u4) column
 // slice [c0, c0+n) -> prepared tiles.
 cudaError_t dgq_launch_repack(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int h, int o_full, int g,

@@ -293,3 +293,95 @@ def test_max_accumulator_at_k28672(cuda):
     assert int(codes_[:, :K].min()) == 127
     _, acc = CL.linear(codes_, rs, out_dtype=torch.float32, want_acc=True)
     assert int(acc.min()) == int(acc.max()) == 28672 * 127 * 127 == 462_450_688
+
+
+@pytest.mark.parametrize("M,K,p", [(37, 7168, 1), (5, 28672, 8), (64, 4096, 2), (3, 100, 1), (9, 96, 4)])
+def test_actq_f16_and_gathered_shards(cuda, port, M, K, p):
+    # FP16 activations (and their all-gathered [p][M][K/p] layout) quantise exactly like float32
+    rng = np.random.default_rng(K + p)
+    x16 = (rng.standard_normal((M, K)) * 3).astype(np.float16)
+    x16[:, 5] *= 40
+    x32 = x16.astype(np.float32)
+    k = rng.uniform(1, 4, K).astype(np.float32)
+    q, rs = port.quantize_activations(x32, k, 1, 0.0)
+    L = dgq.DgqLayer(h=K, o=2, g=K, codes=np.zeros(K, np.uint8), s2=np.ones((1, 2), np.int8),
+                     zp=np.zeros(1, np.uint8), s1=np.ones(2, np.float32), k=k, mode=1)
+    CL = dgq.CudaLayer(L)
+    xd = torch.from_numpy(x16).cuda()
+    if p == 1:
+        codes, drs = CL.quantize_act(xd)
+    else:
+        shards = xd.reshape(M, p, K // p).permute(1, 0, 2).contiguous()
+        codes, drs = CL.quantize_act(shards)
+    assert np.array_equal(codes[:, :K].cpu().numpy(), q)
+    assert np.array_equal(bits(drs.cpu().numpy()), bits(rs))
+
+
+def test_hoisted_reciprocal_division_is_ieee(cuda):
+    # K1 divides by k through RN(1/k) + two FMA corrections (numerics.cuh div_k);
+    # it must equal IEEE div.rn on every input (the fallback covers the rest).
+    import ctypes as C
+
+    lib = dgq.lib()
+    f = lib.dgq_debug_div_check
+    f.argtypes = [C.c_void_p] * 4 + [C.c_size_t, C.c_void_p]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    n = 1 << 24
+    bad = 0
+    for trial in range(6):
+        if trial == 0:    # activations-like: normals, wide k
+            x = torch.randn(n, device="cuda", generator=g) * 50
+            k = 1 + torch.rand(n, device="cuda", generator=g) * 100
+        elif trial == 1:  # random bit patterns over the whole finite range
+            bits_ = torch.randint(0, 0x7F800000, (n,), device="cuda", generator=g, dtype=torch.int32)
+            x = bits_.view(torch.float32) * (torch.randint(0, 2, (n,), device="cuda", generator=g) * 2 - 1)
+            kb = torch.randint(0x3F800000, 0x4B800000, (n,), device="cuda", generator=g, dtype=torch.int32)
+            k = kb.view(torch.float32)
+        elif trial == 2:  # fp16-representable activations
+            x = (torch.randn(n, device="cuda", generator=g) * 300).half().float()
+            k = 1 + torch.rand(n, device="cuda", generator=g) * 7
+        elif trial == 3:  # mantissas near all-ones / near one
+            mb = torch.randint(0x7FFF00, 0x800000, (n,), device="cuda", generator=g, dtype=torch.int32)
+            eb = torch.randint(100, 160, (n,), device="cuda", generator=g, dtype=torch.int32) << 23
+            x = (mb | eb).view(torch.float32)
+            k = (torch.randint(0x3F800000, 0x3F800100, (n,), device="cuda", generator=g,
+                               dtype=torch.int32)).view(torch.float32)
+        elif trial == 4:  # tiny and huge magnitudes around the fast-path bounds
+            x = torch.ldexp(torch.rand(n, device="cuda", generator=g) + 0.5,
+                            torch.randint(-130, 130, (n,), device="cuda", generator=g))
+            k = 1 + torch.rand(n, device="cuda", generator=g) * 3
+        else:             # integers divided by small integers (exact and tie-like quotients)
+            x = torch.randint(-2 ** 24, 2 ** 24, (n,), device="cuda", generator=g).float()
+            k = torch.randint(1, 4096, (n,), device="cuda", generator=g).float()
+        x, k = x.contiguous(), k.contiguous()
+        fast, ieee = torch.empty_like(x), torch.empty_like(x)
+        assert f(C.c_void_p(x.data_ptr()), C.c_void_p(k.data_ptr()), C.c_void_p(fast.data_ptr()),
+                 C.c_void_p(ieee.data_ptr()), n, None) == 0
+        torch.cuda.synchronize()
+        same = (fast.view(torch.int32) == ieee.view(torch.int32)) | (torch.isnan(fast) & torch.isnan(ieee))
+        bad += int((~same).sum())
+    assert bad == 0
+
+
+@pytest.mark.parametrize("M", [3, 300])
+def test_actq_extreme_values_and_huge_k(cuda, port, M):
+    # inputs outside the fast division range (tiny / huge / denormal) and k > 2^24
+    K = 2048
+    rng = np.random.default_rng(M)
+    X = (rng.standard_normal((M, K)) * 2).astype(np.float32)
+    X[:, 0] = 1e-35
+    X[:, 1] = -3e34
+    X[:, 2] = 1e-40  # float32 denormal
+    X[:, 3] = 0.0
+    X[0, 4:40] = np.float32(2.0) ** rng.integers(-120, 120, 36)
+    k = rng.uniform(1, 4, K).astype(np.float32)
+    k[5] = 3.0e7
+    k[6] = 1.0e20
+    for mode, act in ((1, 0.0), (0, 1e-3)):
+        q, rs = port.quantize_activations(X, k, mode, act)
+        L = dgq.DgqLayer(h=K, o=2, g=K, codes=np.zeros(K, np.uint8), s2=np.ones((1, 2), np.int8),
+                         zp=np.zeros(1, np.uint8), s1=np.ones(2, np.float32), k=k, act_scale=act, mode=mode)
+        CL = dgq.CudaLayer(L)
+        codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+        assert np.array_equal(codes[:, :K].cpu().numpy(), q)
+        assert np.array_equal(bits(drs.cpu().numpy()), bits(rs))
