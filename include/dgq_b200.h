@@ -9,9 +9,10 @@
  * offending DgqLayer field for DGQ_EVALIDATION (mirrors dgq::validation_error).
  *
  * The C++ operator API of the reference (proj/include/dgq/kernel.hpp,
- * proj/include/dgq/format.hpp) is implemented on top of these entry points by
- * paper_2310_04836_b200/csrc/dropin.cpp (include/dgq/*.hpp).  Status codes map
- * back to the reference's exception taxonomy:
+ * proj/include/dgq/format.hpp) is implemented on top of the host-buffer entry
+ * points below by paper_2310_04836_b200/dropin/dgq_kernel_b200.cpp, compiled
+ * against the reference's own, unchanged headers.  Status codes map back to
+ * the reference's exception taxonomy:
  *   DGQ_EINVAL      -> std::invalid_argument   (proj/src/kernel.cpp:15-19,47-54,92-98)
  *   DGQ_EVALIDATION -> dgq::validation_error   (proj/src/format.cpp:18-20,131-136)
  *   DGQ_EOVERFLOW   -> std::runtime_error      (proj/src/kernel.cpp:83-85)
@@ -159,6 +160,44 @@ dgq_status dgq_epilogue(const int32_t* dAcc, size_t lda, const float* dRowScale,
 /* ---- audit: max over (r,c,i) of |running sum| (proj/src/kernel.cpp:73-77) --- */
 dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K,
                                  size_t N, int64_t* max_abs_acc, void* stream);
+
+/* ---- host-buffer API: the reference's calling convention --------------------
+ * Host arrays in (reference layouts), host arrays out; each call uploads,
+ * runs the CUDA kernels on a per-thread stream of the CURRENT device and
+ * synchronises.  These are what the C++ drop-in for proj/include/dgq/kernel.hpp
+ * (paper_2310_04836_b200/dropin/) and FFI bindings call.  Row-major, dense. */
+/* quantize_activations, proj/src/kernel.cpp:14-44: X [M x K] -> codes [M x K], row_scales [M] */
+dgq_status dgq_host_quantize_activations(const float* X, size_t M, size_t K, const float* k, int mode,
+                                         float act_scale, int8_t* codes, float* row_scales);
+/* dequantize_to_s8, proj/src/format.cpp:122-141 (DGQ_EVALIDATION field "codes" on corruption) */
+dgq_status dgq_host_dequantize_to_s8(size_t h, size_t o, size_t g, const uint8_t* codes_u4, const int8_t* s2,
+                                     const uint8_t* zp_u4, int8_t* w_s8);
+/* dequantize_to_f32, proj/src/format.cpp:143-154 */
+dgq_status dgq_host_dequantize_to_f32(size_t h, size_t o, size_t g, const uint8_t* codes_u4, const int8_t* s2,
+                                      const uint8_t* zp_u4, const float* s1, float* w);
+/* int8_gemm, proj/src/kernel.cpp:46-87: Xq [M x K] x W [K x N] -> acc [M x N];
+ * max_abs_acc (may be NULL) = the reference's running-sum audit */
+dgq_status dgq_host_int8_gemm(const int8_t* Xq, const int8_t* W, size_t M, size_t K, size_t N, int32_t* acc,
+                              int64_t* max_abs_acc);
+/* epilogue, proj/src/kernel.cpp:89-116 (bias may be NULL) -> y f32 [M x N] */
+dgq_status dgq_host_epilogue(const int32_t* acc, const float* row_scales, const float* s1, const float* bias,
+                             size_t M, size_t N, int fp16_mode, float* y);
+/* segmented_gemm_reference, proj/src/kernel.cpp:118-142 (group-wise comparator) */
+dgq_status dgq_host_segmented_gemm(const int8_t* Xq, const float* row_scales, size_t M, size_t h, size_t o, size_t g,
+                                   const uint8_t* codes_u4, const int8_t* s2, const uint8_t* zp_u4, const float* s1,
+                                   float* y);
+/* dgq_forward, proj/src/kernel.cpp:144-153: the whole path per call (dequant with
+ * range check, K1, fused K5 with FP32 out, audit).  w_s8, act_codes,
+ * row_scales, max_abs_acc may be NULL (not returned). */
+dgq_status dgq_host_forward(size_t M, size_t h, size_t o, size_t g, int mode, float act_scale,
+                            const uint8_t* codes_u4, const int8_t* s2, const uint8_t* zp_u4, const float* s1,
+                            const float* k, const float* X, const float* bias, float* out, int8_t* w_s8,
+                            int8_t* act_codes, float* row_scales, int64_t* max_abs_acc);
+/* Prepared-layer forward with HOST buffers (the serving call): X host f32
+ * [M x h] -> Y host [M x o] (out_dtype); dBias is a DEVICE pointer or NULL.
+ * stream NULL = the per-thread stream.  Synchronises before returning. */
+dgq_status dgq_layer_forward_host(const dgq_layer* layer, const float* X, size_t M, const float* dBias,
+                                  int out_dtype, void* Y, void* stream);
 
 #ifdef __cplusplus
 }

@@ -79,6 +79,16 @@ _SIGS = {
     "dgq_int8_gemm": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, _vp, _sz, C.POINTER(C.c_int64), _vp]),
     "dgq_epilogue": (_i, [_vp, _sz, _vp, _vp, _vp, _sz, _sz, _i, _i, _vp, _sz, _vp]),
     "dgq_audit_max_abs_acc": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, C.POINTER(C.c_int64), _vp]),
+    # host-buffer API (the reference's calling convention)
+    "dgq_host_quantize_activations": (_i, [_vp, _sz, _sz, _vp, _i, _f, _vp, _vp]),
+    "dgq_host_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp]),
+    "dgq_host_dequantize_to_f32": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
+    "dgq_host_int8_gemm": (_i, [_vp, _vp, _sz, _sz, _sz, _vp, C.POINTER(C.c_int64)]),
+    "dgq_host_epilogue": (_i, [_vp, _vp, _vp, _vp, _sz, _sz, _i, _vp]),
+    "dgq_host_segmented_gemm": (_i, [_vp, _vp, _sz, _sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
+    "dgq_host_forward": (_i, [_sz, _sz, _sz, _sz, _i, _f, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              C.POINTER(C.c_int64)]),
+    "dgq_layer_forward_host": (_i, [_vp, _vp, _sz, _vp, _i, _vp, _vp]),
 }
 
 _lock = threading.Lock()

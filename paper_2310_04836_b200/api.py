@@ -370,9 +370,52 @@ def dequantize_to_s8(layer: DgqLayer) -> np.ndarray:
 
 
 def dequantize_to_f32(layer: DgqLayer) -> np.ndarray:
-    """proj/src/format.cpp:143-154: float(double(s1[c]) * double(W_s8))."""
-    w = dequantize_to_s8(layer).astype(np.float64)
-    return (np.asarray(layer.s1, np.float64)[None, :] * w).astype(np.float32)
+    """proj/src/format.cpp:143-154: float(double(s1[c]) * double(W_s8)), on the GPU."""
+    codes, s2, zp, s1, _ = layer.arrays()
+    _dev()
+    w = np.empty((layer.h, layer.o), np.float32)
+    check(lib().dgq_host_dequantize_to_f32(layer.h, layer.o, layer.g, _np_ptr(codes), _np_ptr(s2), _np_ptr(zp),
+                                           _np_ptr(s1), _np_ptr(w)))
+    return w
+
+
+def segmented_gemm_reference(act: ActQuant, layer: DgqLayer) -> np.ndarray:
+    """proj/src/kernel.cpp:118-142: the group-wise (segmented) comparator —
+    per-group exact integer partials x S2, f32-accumulated in group order, then
+    x row scale x s1 — computed by a CUDA kernel."""
+    codes_x = np.ascontiguousarray(act.codes, np.int8)
+    if codes_x.shape[1] != layer.h:
+        raise InvalidArgument(_lib.DGQ_EINVAL, "activation shape mismatch")
+    rs = np.ascontiguousarray(act.row_scales, np.float32)
+    codes, s2, zp, s1, _ = layer.arrays()
+    _dev()
+    M = codes_x.shape[0]
+    y = np.empty((M, layer.o), np.float32)
+    check(lib().dgq_host_segmented_gemm(_np_ptr(codes_x), _np_ptr(rs), M, layer.h, layer.o, layer.g, _np_ptr(codes),
+                                        _np_ptr(s2), _np_ptr(zp), _np_ptr(s1), _np_ptr(y)))
+    return y
+
+
+def host_forward(X, layer: DgqLayer, bias=None) -> ForwardResult:
+    """dgq_forward through the host-buffer C ABI (dgq_host_forward): the exact
+    call the C++ drop-in (paper_2310_04836_b200/dropin/) makes."""
+    X = np.ascontiguousarray(X, np.float32)
+    if X.shape[1] != layer.h:
+        raise InvalidArgument(_lib.DGQ_EINVAL, f"activation columns {X.shape[1]} != layer h {layer.h}")
+    codes, s2, zp, s1, k = layer.arrays()
+    _dev()
+    M = X.shape[0]
+    b = None if bias is None or len(bias) == 0 else np.ascontiguousarray(bias, np.float32)
+    out = np.empty((M, layer.o), np.float32)
+    w = np.empty((layer.h, layer.o), np.int8)
+    q = np.empty((M, layer.h), np.int8)
+    rs = np.empty(M, np.float32)
+    mx = C.c_int64(0)
+    check(lib().dgq_host_forward(M, layer.h, layer.o, layer.g, int(layer.mode), float(layer.act_scale),
+                                 _np_ptr(codes), _np_ptr(s2), _np_ptr(zp), _np_ptr(s1), _np_ptr(k), _np_ptr(X),
+                                 None if b is None else _np_ptr(b), _np_ptr(out), _np_ptr(w), _np_ptr(q), _np_ptr(rs),
+                                 C.byref(mx)))
+    return ForwardResult(out, w, ActQuant(q, rs), int(mx.value))
 
 
 def dgq_forward(X, layer: DgqLayer, bias=None, threads: int = 0) -> ForwardResult:

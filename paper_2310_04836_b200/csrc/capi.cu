@@ -118,6 +118,10 @@ int dgq_abi_version(void) { return DGQ_B200_ABI_VERSION; }
 /* not in the public header: profiling hook for tools/ (device buffer of [cta][8] u64, or NULL) */
 void dgq_debug_set_timestamps(void* d_buf) { g_dbg_ts = static_cast<unsigned long long*>(d_buf); }
 const char* dgq_last_error(void) { return t_msg.c_str(); }
+/* not in the public header: lets the other translation units of the library set the thread-local error */
+dgq_status dgq_internal_fail(dgq_status st, const char* msg, const char* field) {
+  return fail(st, msg ? msg : "", field ? field : "");
+}
 const char* dgq_last_error_field(void) { return t_field.c_str(); }
 
 dgq_status dgq_clip_interval(int s2, int zp, int* lo, int* hi) {

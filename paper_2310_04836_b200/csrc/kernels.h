@@ -106,3 +106,10 @@ cudaError_t dgq_launch_epilogue(const int32_t* acc, size_t lda, const float* rs,
 // max over (r, c, i) of |prefix sum| (proj/src/kernel.cpp:73-77); *out must be 0.
 cudaError_t dgq_launch_audit(const int8_t* Xq, size_t ldx, const int8_t* W, size_t ldw, int M, int K, int N,
                              unsigned long long* out, cudaStream_t st);
+// segmented_gemm_reference comparator (proj/src/kernel.cpp:118-142) over the
+// reference layout; y [M x o] f32.
+cudaError_t dgq_launch_segmented(const int8_t* Xq, size_t ldx, const float* rs, const uint8_t* codes,
+                                 const int8_t* s2, const uint8_t* zp, const float* s1, int M, int h, int o, int g,
+                                 float* y, size_t ldy, cudaStream_t st);
+// dequantize_to_f32 (proj/src/format.cpp:143-154) from W_s8 [h x o].
+cudaError_t dgq_launch_dequant_f32(const int8_t* w, const float* s1, int h, int o, float* out, cudaStream_t st);
