@@ -15,6 +15,8 @@
 #include "../../include/dgq_b200.h"
 #include "kernels.h"
 
+extern "C" int dgq_debug_decode_mode();
+
 namespace {
 
 thread_local std::string t_msg;
@@ -63,6 +65,24 @@ dgq_status make_tmap(CUtensorMap* m, const void* base, size_t rows, size_t cols,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return DGQ_OK;
+}
+
+// 3-D view of the activation codes for the decode kernel: (128 k, rows, k-block)
+// with strides (1, ld, 128) bytes; box = 128 B x box_rows x depth, 128-byte
+// swizzle: one request stages `depth` consecutive k-blocks' [rows x 128] tiles.
+dgq_status make_tmap_kblocks(CUtensorMap* m, const void* base, size_t rows, size_t cols, size_t ld, uint32_t box_rows,
+                             uint32_t depth) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {128u, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 128)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld), 128u};
+  cuuint32_t box[3] = {128u, box_rows, depth};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DGQ_ECUDA, "cuTensorMapEncodeTiled (3-D) failed (" + std::to_string(r) + ")");
   return DGQ_OK;
 }
 
@@ -410,7 +430,7 @@ dgq_status dgq_linear_plan(const dgq_layer* L, size_t M, int* token_tile, int* w
   if (token_tile) *token_tile = pl.bn;
   if (weight_tiles) *weight_tiles = pl.nt;
   if (k_splits) *k_splits = pl.splits;
-  if (ctas) *ctas = pl.m_tiles * ((pl.n_tiles + pl.nt - 1) / pl.nt) * pl.splits;
+  if (ctas) *ctas = pl.decode ? pl.ctas : pl.m_tiles * ((pl.n_tiles + pl.nt - 1) / pl.nt) * pl.splits;
   return DGQ_OK;
 }
 
@@ -476,6 +496,50 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
   CUtensorMap tmB;
   dgq_status ms = make_tmap(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn));
   if (ms != DGQ_OK) return ms;
+  if (pl.decode) {
+    DgqDecodeParams d{};
+    d.tiles = tiles;
+    d.chunk_bytes = static_cast<uint32_t>(dgq_layout::chunk_bytes(g));
+    d.chunk_stride = d.chunk_bytes;
+    d.gpk = g >= 128 ? 1 : 128 / g;
+    d.gshift = 7;
+    if (g < 128) {
+      d.gshift = 0;
+      while ((1 << d.gshift) < g) ++d.gshift;
+    }
+    {
+      // units per stage: as many as the TMEM partial ring allows with >= 2 slots
+      const int per = d.gpk * pl.bn;
+      int ku = 128 / per;
+      const int ups = dgq_decode_units_per_stage(pl.bn);
+      d.ku = ku < 1 ? 1 : (ku > ups ? ups : ku);
+      const int room = 256 / (d.ku * per);  // TMEM columns [256, 512) hold the partial ring
+      d.sd_log2 = room >= 8 ? 3 : (room >= 4 ? 2 : (room >= 2 ? 1 : 0));
+    }
+    ms = make_tmap_kblocks(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn), static_cast<uint32_t>(d.ku));
+    if (ms != DGQ_OK) return ms;
+    d.M = static_cast<int>(M);
+    d.N = static_cast<int>(N);
+    d.n_tiles = pl.n_tiles;
+    d.k_blocks = static_cast<int>(k_pad / 128);
+    d.rs = dRs;
+    d.s1 = dS1;
+    d.bias = dBias;
+    d.out = dY;
+    d.ldy = ldy;
+    d.out_f16 = out_dtype == DGQ_OUT_F16;
+    d.fp16_mode = fp16_mode;
+    d.acc_out = dAcc;
+    d.ld_acc = ld_acc;
+    d.ws = static_cast<int32_t*>(ws);
+    d.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
+    if (!ws) return fail(DGQ_EINVAL, "decode kernel needs a workspace");
+    d.dbg = dgq_debug_decode_mode() >> 1;
+    d.trace = g_dbg_ts;
+    d.trace_cta = 0;
+    DGQ_CUDA(dgq_launch_decode(pl.bn, tmB, d, pl.ctas, pl.pdl != 0, st));
+    return DGQ_OK;
+  }
   DgqGemmParams p{};
   p.tiles = tiles;
   p.chunk_bytes = static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128));

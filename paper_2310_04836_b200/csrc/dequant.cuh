@@ -17,16 +17,16 @@ __device__ __forceinline__ uint32_t dq_bias2(uint32_t s2, uint32_t zp) {
   return a | (a << 16);
 }
 
-// word nibble layout: k0 k1 k4 k5 | k2 k3 k6 k7 at nibbles 0,1,2,3,4,5,6,7 as
-// {0:k0, 1:k1, 2:k4, 3:k5, 4:k2, 5:k3, 6:k6, 7:k7}; lo = bytes k0..k3, hi = k4..k7.
+// word nibble layout (kernels.h kNibblePos): nibble 2j = k j, nibble 2j+1 = k j+4,
+// i.e. {0:k0, 1:k4, 2:k1, 3:k5, 4:k2, 5:k6, 6:k3, 7:k7}; lo = bytes k0..k3, hi = k4..k7.
 __device__ __forceinline__ void dq_word(uint32_t w, uint32_t s2, uint32_t bias2, uint32_t& lo, uint32_t& hi) {
   const uint32_t m = 0x000F000Fu;
   const uint32_t v0 = (w & m) * s2 + bias2;
   const uint32_t v1 = ((w >> 4) & m) * s2 + bias2;
   const uint32_t v2 = ((w >> 8) & m) * s2 + bias2;
   const uint32_t v3 = ((w >> 12) & m) * s2 + bias2;
-  lo = __byte_perm(v0, v1, 0x6240);
-  hi = __byte_perm(v2, v3, 0x6240);
+  lo = __byte_perm(v0, v2, 0x6240);  // (k0, k1, k2, k3)
+  hi = __byte_perm(v1, v3, 0x6240);  // (k4, k5, k6, k7)
 }
 
 }  // namespace dgqk

@@ -554,9 +554,43 @@ double est_cycles(int M, int N, int kblocks, int bn, int nt, int splits, bool fu
 }
 }  // namespace
 
+namespace {
+int g_decode_mode = 1;  // tools: 0 = never use K5d (A/B comparisons against the prefill orientation)
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+}  // namespace
+
+extern "C" void dgq_debug_set_decode(int mode) { g_decode_mode = mode; }
+extern "C" int dgq_debug_decode_mode() { return g_decode_mode; }
+
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn, int force_splits) {
   DgqGemmPlan pl{};
   const int kblocks = K_pad / 128;
+  const int dec_bn = M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : 64));
+  const int dec_gpk = g >= 128 ? 1 : (g > 0 ? 128 / g : 1);
+  if (fused && g >= 32 && g % 32 == 0 && M <= 64 && dec_bn * dec_gpk <= 128 && g_decode_mode && !force_bn &&
+      !force_splits) {
+    // K5d: weight-streaming decode kernel, one persistent CTA per SM (stream-K)
+    pl.decode = 1;
+    pl.bn = dec_bn;
+    pl.nt = 1;
+    pl.m_tiles = 1;
+    pl.n_tiles = (N + 127) / 128;
+    pl.splits = 1;
+    pl.kb_per_split = kblocks;
+    const long long units = static_cast<long long>(pl.n_tiles) * kblocks;
+    pl.ctas = static_cast<int>(units < sm_count() ? units : sm_count());
+    const uint32_t cs = static_cast<uint32_t>(dgq_layout::chunk_bytes(g));
+    pl.smem_bytes = dgq_decode_smem_bytes(pl.bn, dgq_decode_stages(pl.bn), cs);
+    pl.ws_bytes = static_cast<size_t>(pl.n_tiles) * pl.bn * 128 * 4;
+    pl.counter_bytes = static_cast<size_t>(pl.n_tiles) * 4;
+    pl.est_cycles = 0;
+    pl.pdl = 1;
+    return pl;
+  }
   const uint32_t cs = (dgq_layout::chunk_bytes(g > 0 ? g : 128) + 1023) & ~1023u;
   double best = 1e30;
   int bbn = 0, bnt = 1, bsp = 1;

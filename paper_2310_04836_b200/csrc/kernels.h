@@ -10,8 +10,12 @@
 // k-blocks.  Every (n-tile, k-block) owns one contiguous chunk in HBM:
 //   [0, 8192)            packed INT4 codes: for j in 0..3 (32-k slice), for n in
 //                        0..127: 16 B = 4 words of 8 k each.  Inside a word the
-//                        k-offset t sits in nibble kNibblePos[t], the order the
-//                        in-kernel IMAD/PRMT dequantiser emits bytes in.
+//                        k-offset t sits in nibble kNibblePos[t]: byte j holds
+//                        k = j (low nibble) and k = j + 4 (high nibble), so
+//                        `w & 0x0F0F0F0F` / `(w >> 4) & 0x0F0F0F0F` are the
+//                        raw codes of k 0..3 / 4..7 in order (decode kernel),
+//                        and the IMAD/PRMT dequantiser (dequant.cuh) pairs
+//                        16-bit lanes (k0,k2)+(k1,k3) and (k4,k6)+(k5,k7).
 //   [8192, 8192+256*gpk) per-group scales: for each group overlapping the
 //                        k-block, 128 x u16 (S2 | ZP << 8).
 // Chunks are ordered n-tile major so one CTA streams a contiguous range.
@@ -19,7 +23,7 @@ namespace dgq_layout {
 constexpr int kTileN = 128;
 constexpr int kBlockK = 128;
 constexpr int kCodeBytes = 8192;
-constexpr int kNibblePos[8] = {0, 1, 4, 5, 2, 3, 6, 7};
+constexpr int kNibblePos[8] = {0, 2, 4, 6, 1, 3, 5, 7};
 inline int groups_per_kblock(int g) { return g >= kBlockK ? 1 : kBlockK / g; }
 inline int chunk_bytes(int g) { return kCodeBytes + 256 * groups_per_kblock(g); }
 // The fused path needs every 8-k word inside one group and whole groups per
@@ -55,7 +59,41 @@ struct DgqGemmParams {
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
 };
 
+// K5d (decode.cu): stream-K over (weight tile, k-block) units, raw codes as
+// the unsigned A operand from TMEM, group scales applied to TMEM partials.
+struct DgqDecodeParams {
+  const uint8_t* tiles;
+  uint32_t chunk_bytes;
+  uint32_t chunk_stride;
+  int gpk;     // groups per k-block: 1 (g >= 128), 2 (g = 64), 4 (g = 32)
+  int gshift;  // log2(g) for g < 128, else 7
+  int sd_log2; // log2 of the TMEM partial slots (<= 8 slots)
+  int ku;      // units (k-blocks of one tile) per pipeline stage, <= dgq_decode_units_per_stage
+  int M, N, n_tiles, k_blocks;
+  const float* rs;
+  const float* s1;
+  const float* bias;
+  void* out;
+  size_t ldy;
+  int out_f16;
+  int fp16_mode;
+  int32_t* acc_out;
+  size_t ld_acc;
+  int32_t* ws;         // [n_tiles][bn][128] int32, zero on entry and exit
+  uint32_t* counters;  // [n_tiles], zero on entry and exit
+  int dbg;             // tools only: bit0 skip MMA, bit1 skip unpack, bit2 skip epilogue math
+  unsigned long long* trace;  // tools only: [4 roles][1024 units] globaltimer stamps of CTA `trace_cta`
+  int trace_cta;
+};
+size_t dgq_decode_smem_bytes(int bn, int sl, uint32_t chunk_stride);
+int dgq_decode_stages(int bn);            // units of shared-memory ring (stages x units per stage)
+int dgq_decode_units_per_stage(int bn);   // box depth of the 3-D Xq tensor map
+cudaError_t dgq_launch_decode(int bn, const CUtensorMap& tmB, const DgqDecodeParams& p, int grid, bool pdl,
+                              cudaStream_t st);
+
 struct DgqGemmPlan {
+  int decode;  // 1: K5d (decode.cu) with token tile bn, `ctas` persistent CTAs
+  int ctas;
   int bn;
   int nt;  // 128-row weight tiles per CTA
   int m_tiles, n_tiles, splits, kb_per_split;

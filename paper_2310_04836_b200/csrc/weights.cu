@@ -15,7 +15,7 @@ __device__ __forceinline__ uint32_t ref_nibble(const uint8_t* p, size_t idx) {
   return (idx & 1) ? (b >> 4) : (b & 0x0Fu);
 }
 
-__constant__ int c_nib_pos[8] = {0, 1, 4, 5, 2, 3, 6, 7};
+__constant__ int c_nib_pos[8] = {0, 2, 4, 6, 1, 3, 5, 7};
 
 // one thread per (n-tile, k-block, j, n): 32 codes -> 16 bytes (+ scales when j == 0)
 __global__ void k_repack(const uint8_t* __restrict__ codes, const int8_t* __restrict__ s2,

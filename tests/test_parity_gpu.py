@@ -241,17 +241,65 @@ def test_fp16_mode_epilogue_in_fused_kernel(cuda, port):
 
 
 @pytest.mark.parametrize("M", [1, 4, 16, 48])
-def test_cluster_split_k_is_exact_and_repeatable(cuda, port, M):
-    # decode shapes run split-K through the int32 workspace; run twice to check it is left zeroed
+def test_decode_stream_k_is_exact_and_repeatable(cuda, port, M):
+    # decode shapes (M <= 64) run K5d: persistent CTAs split the (tile, k-block)
+    # units evenly, partial tiles are reduced exactly through the int32 workspace;
+    # run three times to check the workspace and tile counters are left zeroed
     L = oracle.random_layer(4096, 256, 128, seed=M)
     X = port.gen_synthetic(M, 4096, M, 3, 50.0, 3)
     out, w, q, rs, mx = port.dgq_forward(X, L)
     CL = dgq.CudaLayer(_to_dgq(L))
-    assert CL.plan(M)["k_splits"] > 1  # decode shapes reduce K over a thread-block cluster
+    plan = CL.plan(M)
+    assert plan["ctas"] > 2  # 2 tiles x 32 k-blocks spread over many CTAs: every tile is split
     codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
     for _ in range(3):
         y = CL.linear(codes, drs, out_dtype=torch.float32)
         assert np.array_equal(bits(y.cpu().numpy()), bits(out))
+
+
+DECODE_CASES = [
+    # (M, h, o, g): token tiles 8/16/32/64, g = 32/64/128/256, ragged h and o
+    (1, 7168, 1024, 128), (8, 1024, 130, 128), (9, 2048, 640, 64), (17, 4096, 384, 32), (33, 1920, 256, 128),
+    (64, 8192, 512, 256), (2, 384, 2, 32), (5, 28672, 256, 128), (64, 640, 4000, 64),
+]
+
+
+@pytest.mark.parametrize("M,h,o,g", DECODE_CASES)
+def test_decode_kernel_matches_oracle(cuda, port, M, h, o, g):
+    L = oracle.random_layer(h, o, g, seed=M + h + o + g)
+    X = port.gen_synthetic(M, h, 5 + M, 3, 50.0, 3)
+    bias = np.random.default_rng(M).uniform(-0.5, 0.5, o).astype(np.float32)
+    out, w, q, rs, mx = port.dgq_forward(X, L, bias)
+    acc_ref, _ = port.int8_gemm(q, w)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+    db = torch.from_numpy(bias).cuda()
+    for _ in range(2):
+        y32, acc = CL.linear(codes, drs, bias=db, out_dtype=torch.float32, want_acc=True)
+        assert np.array_equal(acc.cpu().numpy(), acc_ref)
+        assert np.array_equal(bits(y32.cpu().numpy()), bits(out))
+    y16 = CL.linear(codes, drs, bias=db, out_dtype=torch.float16)
+    assert np.array_equal(bits(y16.cpu().numpy()), bits(port.fp16_round_array(out).astype(np.float16)))
+    yf = CL.linear(codes, drs, out_dtype=torch.float32, fp16_mode=True)
+    assert np.array_equal(bits(yf.cpu().numpy()), bits(port.epilogue(acc_ref, rs, L.s1, None, True)))
+
+
+def test_decode_and_prefill_orientations_agree(cuda, port):
+    import ctypes
+
+    L = oracle.random_layer(2048, 512, 64, seed=11)
+    X = port.gen_synthetic(24, 2048, 4, 3, 50.0, 3)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+    lib = dgq.lib()
+    lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    a = CL.linear(codes, drs, out_dtype=torch.float32).cpu().numpy()
+    lib.dgq_debug_set_decode(0)
+    try:
+        b = CL.linear(codes, drs, out_dtype=torch.float32).cpu().numpy()
+    finally:
+        lib.dgq_debug_set_decode(1)
+    assert np.array_equal(bits(a), bits(b))
 
 
 def test_column_shards_concatenate_to_full(cuda, port):
