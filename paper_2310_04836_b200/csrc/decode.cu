@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
   const int KB = p.k_blocks;
   const int ku = p.ku;                   // units per stage (<= UPS)
   const int gpk = p.gpk;                 // groups per k-block (1, 2 or 4)
+  const int gpk_log2 = gpk >> 1;         // 1 -> 0, 2 -> 1, 4 -> 2
   const int dslot = ku * gpk * BN;       // TMEM columns of one stage's partials
   const int sdl = p.sd_log2;             // partial slots = 1 << sdl
   const long long U = static_cast<long long>(p.n_tiles) * KB;
@@ -222,8 +223,12 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
     // issue alternate units of each stage.  The unpack warps arrive on afull
     // only after they waited for the stage's TMA (full), so afull also orders
     // the Xq tile before the MMA reads it.
-    if (lane == 0) {
+    // The whole warp runs the loop converged and one lane is elected inside
+    // the MMA/commit asm: the operands stay in uniform registers, which takes
+    // the issue cost from ~50 to ~24 cycles per MMA (tools/tc_probe2.cu).
+    {
       const int mw = warp - 1;
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       uint32_t qoff[4], acc_in[4];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
@@ -240,16 +245,16 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
         tc_fence_after();
         for (int c = mw; c < w.cnt; c += kMmaWarps) {
           const uint64_t db = umma_desc_sw128(smem_u32(sB + (s * UPS + c) * kBBytes));
-          const uint32_t a0 = tmem + (sa * UPS + c) * 32;
-          const uint32_t d0 = tmem + kDCol0 + sd * dslot + c * unit_dcols;
+          const uint32_t a0 = tm + (sa * UPS + c) * 32;
+          const uint32_t d0 = tm + kDCol0 + sd * dslot + c * unit_dcols;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)  // K = 32 per MMA: +8 TMEM columns of A, +32 B of the B row
-            mma_i8_ts(d0 + qoff[kk], a0 + kk * 8, db + 2 * kk, kIdesc, acc_in[kk]);
+            mma_i8_ts_warp(d0 + qoff[kk], a0 + kk * 8, db + 2 * kk, kIdesc, acc_in[kk]);
         }
-        mma_commit(&empty[s]);
-        mma_commit(&aempty[sa]);
-        mma_commit(&dfull[sd]);
-        if (mw == 0) dec::trace_stamp(p, 1, i);
+        mma_commit_warp(&empty[s]);
+        mma_commit_warp(&aempty[sa]);
+        mma_commit_warp(&dfull[sd]);
+        if (mw == 0 && lane == 0) dec::trace_stamp(p, 1, i);
       }
     }
     __syncwarp();
@@ -259,31 +264,46 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
     const int row = (warp & 3) * 32 + lane;     // output channel inside the tile == TMEM lane
     const int half = (warp - 4) >> 2;           // which 64-k half of the row
     const uint32_t taddr_lane = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int q0h = p.gshift >= 7 ? 0 : ((half * 64) >> p.gshift);       // group of k [64h, 64h+32)
+    const int q1h = p.gshift >= 7 ? 0 : ((half * 64 + 32) >> p.gshift);  // group of k [64h+32, 64h+64)
     StageWalk w;
     for (w.init(u0, nu, KB, ku); w.valid(); w.next(KB, ku)) {
       const int i = w.idx, s = i % SL, sa = i % kSA;
       mbar_wait(&full[s], (i / SL) & 1);
       mbar_wait(&aempty[sa], ((i / kSA) & 1) ^ 1);
-      for (int c = 0; c < w.cnt; ++c) {
-        // 64 codes of channel `row`: [j][row][16 B]; byte b of word w = k(8w+b) | k(8w+b+4) << 4
-        const uint8_t* chunk = sC + s * stage_cb + c * p.chunk_bytes;
-        const uint16_t* sc = reinterpret_cast<const uint16_t*>(chunk + 8192);
-        const uint4 w0 = *reinterpret_cast<const uint4*>(chunk + (half * 2) * 2048 + row * 16);
-        const uint4 w1 = *reinterpret_cast<const uint4*>(chunk + (half * 2 + 1) * 2048 + row * 16);
-        // zero points of the (up to two) groups of this 64-k half, replicated to 4 bytes
-        const int q0 = p.gshift >= 7 ? 0 : ((half * 64) >> p.gshift);
-        const int q1 = p.gshift >= 7 ? 0 : ((half * 64 + 32) >> p.gshift);
-        const uint32_t z0 = (static_cast<uint32_t>(sc[q0 * 128 + row]) >> 8) * 0x01010101u;
-        const uint32_t z1 = (static_cast<uint32_t>(sc[q1 * 128 + row]) >> 8) * 0x01010101u;
-        const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        uint32_t a[16];
+      // all of the stage's loads first (one shared-memory round trip), then the
+      // byte arithmetic and one tcgen05.st per unit
+      const uint8_t* stage_c = sC + s * stage_cb;
+      uint4 cw[UPS][2];
+      uint32_t zz[UPS][2];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t z = k < 4 ? z0 : z1;
-          a[2 * k] = (((wv[k] & 0x0F0F0F0Fu) | 0x80808080u) - z) ^ 0x80808080u;
-          a[2 * k + 1] = ((((wv[k] >> 4) & 0x0F0F0F0Fu) | 0x80808080u) - z) ^ 0x80808080u;
+      for (int c = 0; c < UPS; ++c) {
+        if (c < w.cnt) {
+          // 64 codes of channel `row`: [j][row][16 B]; byte b of word w = k(8w+b) | k(8w+b+4) << 4
+          const uint8_t* chunk = stage_c + c * p.chunk_bytes;
+          const uint16_t* sc = reinterpret_cast<const uint16_t*>(chunk + 8192);
+          cw[c][0] = *reinterpret_cast<const uint4*>(chunk + (half * 2) * 2048 + row * 16);
+          cw[c][1] = *reinterpret_cast<const uint4*>(chunk + (half * 2 + 1) * 2048 + row * 16);
+          // zero points of the (up to two) groups of this 64-k half
+          zz[c][0] = sc[q0h * 128 + row] >> 8;
+          zz[c][1] = sc[q1h * 128 + row] >> 8;
         }
-        tmem_st16(tmem + taddr_lane + (sa * UPS + c) * 32 + half * 16, a);
+      }
+#pragma unroll
+      for (int c = 0; c < UPS; ++c) {
+        if (c < w.cnt) {
+          const uint32_t z0 = zz[c][0] * 0x01010101u, z1 = zz[c][1] * 0x01010101u;
+          const uint32_t wv[8] = {cw[c][0].x, cw[c][0].y, cw[c][0].z, cw[c][0].w,
+                                  cw[c][1].x, cw[c][1].y, cw[c][1].z, cw[c][1].w};
+          uint32_t a[16];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t z = k < 4 ? z0 : z1;
+            a[2 * k] = (((wv[k] & 0x0F0F0F0Fu) | 0x80808080u) - z) ^ 0x80808080u;
+            a[2 * k + 1] = ((((wv[k] >> 4) & 0x0F0F0F0Fu) | 0x80808080u) - z) ^ 0x80808080u;
+          }
+          tmem_st16(tmem + taddr_lane + (sa * UPS + c) * 32 + half * 16, a);
+        }
       }
       tmem_st_wait();
       tc_fence_before();
@@ -313,13 +333,14 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
       // themselves in 32-column TMEM loads (column j = (unit * gpk + group) * BN + token)
       int32_t s2v[UPS * 4];
       const int ncq = w.cnt * gpk;
+      const uint16_t* sc0 = reinterpret_cast<const uint16_t*>(sC + s * stage_cb + 8192) + e;
+      const int cstride = static_cast<int>(p.chunk_bytes >> 1);  // u16 stride between the stage's chunks
 #pragma unroll
       for (int cq = 0; cq < UPS * 4; ++cq) {
         s2v[cq] = 0;
         if (cq < ncq) {
-          const int c = cq / gpk, q = cq - c * gpk;
-          s2v[cq] = static_cast<int32_t>(
-              reinterpret_cast<const uint16_t*>(sC + s * stage_cb + c * p.chunk_bytes + 8192)[q * 128 + e] & 0xFFu);
+          const int c = cq >> gpk_log2, q = cq & (gpk - 1);
+          s2v[cq] = static_cast<int32_t>(sc0[c * cstride + q * 128] & 0xFFu);
         }
       }
       const uint32_t dcol = tmem + lane_base + kDCol0 + sd * dslot;

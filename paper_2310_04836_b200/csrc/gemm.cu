@@ -571,7 +571,8 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
   const int kblocks = K_pad / 128;
   const int dec_bn = M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : 64));
   const int dec_gpk = g >= 128 ? 1 : (g > 0 ? 128 / g : 1);
-  if (fused && g >= 32 && g % 32 == 0 && M <= 64 && dec_bn * dec_gpk <= 128 && g_decode_mode && !force_bn &&
+  // K5d wins up to 32 tokens; at 33..64 the weight-tile-per-CTA kernel below is faster
+  if (fused && g >= 32 && g % 32 == 0 && M <= 32 && dec_bn * dec_gpk <= 128 && g_decode_mode && !force_bn &&
       !force_splits) {
     // K5d: weight-streaming decode kernel, one persistent CTA per SM (stream-K)
     pl.decode = 1;

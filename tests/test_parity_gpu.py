@@ -240,7 +240,7 @@ def test_fp16_mode_epilogue_in_fused_kernel(cuda, port):
     assert np.array_equal(bits(y.cpu().numpy()), bits(ref))
 
 
-@pytest.mark.parametrize("M", [1, 4, 16, 48])
+@pytest.mark.parametrize("M", [1, 4, 16, 32])
 def test_decode_stream_k_is_exact_and_repeatable(cuda, port, M):
     # decode shapes (M <= 64) run K5d: persistent CTAs split the (tile, k-block)
     # units evenly, partial tiles are reduced exactly through the int32 workspace;
@@ -259,8 +259,8 @@ def test_decode_stream_k_is_exact_and_repeatable(cuda, port, M):
 
 DECODE_CASES = [
     # (M, h, o, g): token tiles 8/16/32/64, g = 32/64/128/256, ragged h and o
-    (1, 7168, 1024, 128), (8, 1024, 130, 128), (9, 2048, 640, 64), (17, 4096, 384, 32), (33, 1920, 256, 128),
-    (64, 8192, 512, 256), (2, 384, 2, 32), (5, 28672, 256, 128), (64, 640, 4000, 64),
+    (1, 7168, 1024, 128), (8, 1024, 130, 128), (9, 2048, 640, 64), (17, 4096, 384, 32), (32, 1920, 256, 128),
+    (31, 8192, 512, 256), (2, 384, 2, 32), (5, 28672, 256, 128), (24, 640, 4000, 64), (33, 1024, 512, 128),
 ]
 
 

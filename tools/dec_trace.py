@@ -1,5 +1,7 @@
-"""Per-role timeline of CTA 0 of one K5d launch (globaltimer stamps):
-role 0 producer stage issue, 1 MMA issued, 2 unpack done, 3 epilogue done.
+"""Per-role timeline of CTA 0 of one K5d launch (debug trace buffer):
+rows 0-3 globaltimer stamps (producer stage issue, MMA done, unpack done,
+epilogue done), rows 4-8/12 per-stage cycle counts (when the kernel is built
+with them), row 13 [cycles, ns] of the whole CTA.
 python tools/dec_trace.py M K N [g]"""
 import ctypes as C
 import os
@@ -29,18 +31,21 @@ CL.linear(codes, rs, out=out)
 torch.cuda.synchronize()
 lib.dgq_debug_set_timestamps(None)
 ts = buf.view(16, 1024).cpu().numpy().astype(np.int64)
-t0 = ts[ts > 0].min()
-names = ["producer", "mma_done", "unp_done", "epi_done", "unp_start", "unp_full", "unp_aempty", "unp_xempty",
-         "mma_start", "mma_full", "mma_afull", "mma_dempty", "epi_start", "epi_dfull", "epi_xfull", "-"]
-lab = {4: "mma wait afull", 5: "mma wait dempty", 6: "mma issue", 7: "mma commits", 8: "unp wait full",
-       9: "unp wait aempty", 10: "unp work", 11: "unp st-wait+arrive", 12: "epi wait dfull", 13: "epi work"}
-for r in range(4, 14):
-    print(f"  {lab[r]:20s}", ts[r][2:18].tolist())
+cyc, ns = ts[13][0], ts[13][1]
+print(f"CTA 0: {cyc} cycles in {ns} ns -> {cyc / max(ns, 1) * 1e3:.0f} MHz")
+lab = {4: "mma waits", 5: "mma issue+commit", 6: "unp wait full", 7: "unp wait aempty", 8: "unp work+arrive",
+       12: "epi tmem ld+wait"}
+for r, name in lab.items():
+    if ts[r].any():
+        print(f"  {name:20s}", ts[r][2:18].tolist())
+stamps = ts[0:4]
+t0 = stamps[stamps > 0].min()
+names = ["producer", "mma_done", "unp_done", "epi_done"]
 for r in range(4):
-    v = ts[r][ts[r] > 0]
+    v = stamps[r][stamps[r] > 0]
     if not len(v):
         continue
     v = (v - t0) / 1e3
     d = np.diff(v)
-    print(f"{names[r]:11s} n={len(v):4d} first {v[0]:7.2f} last {v[-1]:7.2f} us  step {np.median(d) if len(d) else 0:6.3f}"
+    print(f"{names[r]:9s} n={len(v):4d} first {v[0]:7.2f} last {v[-1]:7.2f} us  step {np.median(d) if len(d) else 0:6.3f}"
           f"  t[6:12]={np.round(v[6:12], 2).tolist()}")

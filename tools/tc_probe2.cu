@@ -20,7 +20,26 @@ __global__ void k(long long* out, int issuers, int rot) {
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tmem = tslot;
   const int total = 512;
-  if (warp < issuers && lane == 0) {
+  if (warp < issuers && rot == 2) {
+    const uint32_t idesc = idesc_u8s8(128, N);
+    const uint64_t db = umma_desc_sw128(smem_u32(sB));
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const int mine = total / issuers;
+    long long t0 = clk();
+    for (int it = 0; it < mine; ++it) {
+      const int kk = it & 3;
+      const uint32_t d = tm + 256 + warp * 128 + ((it >> 2) & 7) * N;
+      mma_i8_ts_warp(d, tm + warp * 64 + kk * 8, db + 2 * kk, idesc, kk ? 1u : 0u);
+    }
+    long long t1 = clk();
+    mma_commit_warp(&bar[warp]);
+    mbar_wait(&bar[warp], 0);
+    long long t2 = clk();
+    if (lane == 0) {
+      out[warp * 2] = t1 - t0;
+      out[warp * 2 + 1] = t2 - t0;
+    }
+  } else if (warp < issuers && lane == 0) {
     const uint32_t idesc = idesc_u8s8(128, N);
     const uint64_t db = umma_desc_sw128(smem_u32(sB));
     const int mine = total / issuers;
@@ -50,6 +69,6 @@ template <int N> void run(int issuers, int rot) {
   cudaFree(d);
 }
 int main() {
-  for (int rot = 0; rot < 2; ++rot) { run<8>(1, rot); run<8>(2, rot); run<16>(1, rot); run<16>(2, rot); }
+  for (int rot = 1; rot < 3; ++rot) { run<8>(1, rot); run<8>(2, rot); run<16>(1, rot); run<16>(2, rot); }
   return 0;
 }
