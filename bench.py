@@ -302,6 +302,67 @@ def timed_steps(layer, M, steps, warmup, flush, sync_all, e2e=None):
     return times
 
 
+def _graph_of(fn):
+    import torch
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()  # warm: allocates workspaces outside the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def decode_step_time(layer, M, flush, sync_all, world, reps=8):
+    """Mean device time (s) of one decoder-layer step at M tokens."""
+    import torch
+
+    if world > 1:  # collectives stay eager under torchrun
+        t = timed_steps(layer, M, reps, 2, flush, sync_all)
+        return sum(t) / len(t)
+    g = _graph_of(lambda: layer.step(M))
+    times = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        times.append(a.elapsed_time(b) * 1e-3)
+    return sum(times) / len(times)
+
+
+def decode_k5_bandwidth(layer, M, flush, reps=8):
+    """Algorithmic HBM GB/s of each K5 launch at M tokens (graph-replayed, L2 flushed)."""
+    import torch
+
+    out = {}
+    for name, K, N in OPT30B:
+        lin = layer.lin[name]
+        key = "q" if name in ("q", "k", "v") else name
+        codes, rs = layer.codes[key][:M], layer.rs[key][:M]
+        g = _graph_of(lambda: lin.linear(codes, rs, out=layer.y[name][:M]))
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        t = sum(ts) / len(ts)
+        ns = lin.shard
+        byts = M * K + 4 * M + K * ns / 2 + (K / GROUP) * ns * 1.5 + 4 * ns + 2 * M * ns
+        out[name] = byts / t / 1e9
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -393,12 +454,18 @@ def run_ours(args):
             detail[f"tops_seq{M}"] = layer_ops(M) / tm / 1e12
         detail["layer_ms_seq2048"] = ms_per_step
         for M in (1, 16):
-            t = timed_steps(layer, M, 5, 2, flush, sync_all)
-            tm = max_over_ranks(sum(t)) / 5
+            # decode steps are launch-bound from Python: replay the step from a CUDA graph
+            # (single rank) so the number is the GPU's; L2 flushed before every replay
+            tm = decode_step_time(layer, M, flush, sync_all, world)
+            tm = max_over_ranks(tm)
             wb = layer_weight_bytes(world)
             detail[f"decode_m{M}_layer_us"] = tm * 1e6
             detail[f"decode_m{M}_weight_GBps_per_gpu"] = wb / tm / 1e9
             detail[f"decode_m{M}_hbm_frac"] = wb / tm / 1e9 / hbm_peak
+            if world == 1:
+                kb = decode_k5_bandwidth(layer, M, flush)
+                detail[f"decode_m{M}_k5_GBps"] = kb
+                detail[f"decode_m{M}_k5_hbm_frac"] = {n: v / hbm_peak for n, v in kb.items()}
         detail["k5_tops_by_linear"] = {n: o / t / 1e12 for n, (t, o) in by_name.items()}
         detail["k1_GBps"] = k1_b / k1_t / 1e9
         plans = {n: layer.lin[n].layer.plan(SEQ) for n in ("q", "fc1", "fc2")}

@@ -534,7 +534,7 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     d.ws = static_cast<int32_t*>(ws);
     d.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
     if (!ws) return fail(DGQ_EINVAL, "decode kernel needs a workspace");
-    d.dbg = dgq_debug_decode_mode() >> 1;
+    d.dbg = (dgq_debug_decode_mode() >> 1) & 0x7F;
     d.trace = g_dbg_ts;
     d.trace_cta = 0;
     DGQ_CUDA(dgq_launch_decode(pl.bn, tmB, d, pl.ctas, pl.pdl != 0, st));

@@ -167,6 +167,11 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
   uint32_t* s_flag = tmem_slot + 1;
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0 && p.trace && blockIdx.x < 1024) {  // tools only: CTA start stamp
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.trace[14 * 1024 + blockIdx.x] = static_cast<long long>(t);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < SL; ++s) {
       mbar_init(&full[s], 1);
@@ -406,6 +411,11 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && p.trace && blockIdx.x < 1024) {  // tools only: CTA end stamp
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.trace[15 * 1024 + blockIdx.x] = static_cast<long long>(t);
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);

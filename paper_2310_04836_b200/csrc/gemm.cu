@@ -589,7 +589,7 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
     pl.ws_bytes = static_cast<size_t>(pl.n_tiles) * pl.bn * 128 * 4;
     pl.counter_bytes = static_cast<size_t>(pl.n_tiles) * 4;
     pl.est_cycles = 0;
-    pl.pdl = 1;
+    pl.pdl = (g_decode_mode & 0x100) ? 0 : 1;  // tools: mode bit 8 disables PDL
     return pl;
   }
   const uint32_t cs = (dgq_layout::chunk_bytes(g > 0 ? g : 128) + 1023) & ~1023u;

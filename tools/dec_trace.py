@@ -38,6 +38,13 @@ lab = {4: "mma waits", 5: "mma issue+commit", 6: "unp wait full", 7: "unp wait a
 for r, name in lab.items():
     if ts[r].any():
         print(f"  {name:20s}", ts[r][2:18].tolist())
+st, en = ts[14], ts[15]
+ok = (st > 0) & (en > 0)
+if ok.any():
+    s0 = st[ok].min()
+    print(f"CTAs: start {(st[ok].min() - s0) / 1e3:.2f}..{(st[ok].max() - s0) / 1e3:.2f} us, "
+          f"end {(en[ok].min() - s0) / 1e3:.2f}..{(en[ok].max() - s0) / 1e3:.2f} us "
+          f"(median end {(np.median(en[ok]) - s0) / 1e3:.2f})")
 stamps = ts[0:4]
 t0 = stamps[stamps > 0].min()
 names = ["producer", "mma_done", "unp_done", "epi_done"]
