@@ -430,7 +430,7 @@ dgq_status dgq_linear_plan(const dgq_layer* L, size_t M, int* token_tile, int* w
   if (token_tile) *token_tile = pl.bn;
   if (weight_tiles) *weight_tiles = pl.nt;
   if (k_splits) *k_splits = pl.splits;
-  if (ctas) *ctas = pl.decode ? pl.ctas : pl.m_tiles * ((pl.n_tiles + pl.nt - 1) / pl.nt) * pl.splits;
+  if (ctas) *ctas = (pl.decode || pl.prefill2) ? pl.ctas : pl.m_tiles * ((pl.n_tiles + pl.nt - 1) / pl.nt) * pl.splits;
   return DGQ_OK;
 }
 
@@ -578,6 +578,14 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     p.tma_out = 1;
   }
   p.dbg = g_dbg_ts;
+  if (pl.prefill2) {
+    CUtensorMap tmX;
+    ms = make_tmap(&tmX, dXq, M, k_pad, ldq, 128u);
+    if (ms != DGQ_OK) return ms;
+    p.chunk_stride = p.chunk_bytes;
+    DGQ_CUDA(dgq_launch_prefill2(tmX, tmY, p, pl.pdl != 0, st));
+    return DGQ_OK;
+  }
   DGQ_CUDA(dgq_launch_gemm(pl, fused, tmB, tmA, tmY, p, st));
   return DGQ_OK;
 }

@@ -569,6 +569,22 @@ extern "C" int dgq_debug_decode_mode() { return g_decode_mode; }
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn, int force_splits) {
   DgqGemmPlan pl{};
   const int kblocks = K_pad / 128;
+  // K5p is opt-in (tools / tests: mode bit 10) until it beats the one-CTA kernel below
+  if (fused && M >= 256 && (g_decode_mode & 0x400) != 0 && !force_bn && !force_splits &&
+      dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128))) <= 232448) {
+    // K5p: persistent CTA pairs
+    pl.prefill2 = 1;
+    pl.bn = 256;
+    pl.nt = 2;
+    pl.m_tiles = (M + 255) / 256;
+    pl.n_tiles = (N + 127) / 128;
+    pl.splits = 1;
+    pl.kb_per_split = kblocks;
+    pl.ctas = 2 * dgq_prefill2_clusters(M, N);
+    pl.smem_bytes = dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128)));
+    pl.pdl = 1;
+    return pl;
+  }
   const int dec_bn = M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : 64));
   const int dec_gpk = g >= 128 ? 1 : (g > 0 ? 128 / g : 1);
   // K5d wins up to 32 tokens; at 33..64 the weight-tile-per-CTA kernel below is faster

@@ -92,7 +92,8 @@ cudaError_t dgq_launch_decode(int bn, const CUtensorMap& tmB, const DgqDecodePar
                               cudaStream_t st);
 
 struct DgqGemmPlan {
-  int decode;  // 1: K5d (decode.cu) with token tile bn, `ctas` persistent CTAs
+  int decode;    // 1: K5d (decode.cu) with token tile bn, `ctas` persistent CTAs
+  int prefill2;  // 1: K5p (prefill.cu), persistent CTA pairs, 256 x 256 tiles
   int ctas;
   int bn;
   int nt;  // 128-row weight tiles per CTA
@@ -105,6 +106,12 @@ struct DgqGemmPlan {
 };
 
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn = 0, int force_splits = 0);
+
+// K5p (prefill.cu): persistent CTA-pair kernel; tmA = Xq with 128-row boxes.
+size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride);
+int dgq_prefill2_clusters(int M, int N);
+cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
+                                cudaStream_t st);
 
 cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorMap& tmB, const CUtensorMap& tmA,
                             const CUtensorMap& tmY, const DgqGemmParams& p, cudaStream_t st);

@@ -1,0 +1,483 @@
+// K5p — the prefill-shaped (many tokens) fused DGQ linear on sm_100a: a
+// persistent, CTA-PAIR kernel (tcgen05.mma.cta_group::2, M = 256, N = 256).
+//
+// out[m, n] = ((float(acc[m, n]) * rs[m]) * s1[n]) (+ bias[n]),
+// acc[m, n] = sum_k Xq[m, k] * W_s8[k, n],  W_s8 = S2 * (code - ZP)
+// (proj/src/kernel.cpp:144-153; proj/src/format.cpp:129-130).
+//
+// Why a CTA pair: the INT4 -> INT8 dequantisation of the weight operand costs
+// ~13 integer instructions per 8 codes and must keep pace with the tensor
+// pipe.  With cta_group::2 the pair computes a 256-token x 256-channel tile
+// per MMA while each CTA stages only ITS half of each operand: 128 token rows
+// of Xq (TMA) and 128 dequantised channel rows of W_s8 — half the dequant per
+// MMA cycle compared with one CTA doing the same tile.  Each CTA's TMEM holds
+// its 128 tokens x 256 channels, so two accumulators fit in 512 columns and
+// the epilogue of tile t overlaps the main loop of tile t + 1.
+//
+// Per CTA (512 threads), both CTAs of the pair run the same tile sequence:
+//   warp 0      producer: 2-D TMA of its 128 x 128 Xq tile + 1-D bulk copy of
+//               its 128-channel prepared weight chunk per k-block (SL ring).
+//   warp 1      TMEM (cta_group::2 alloc, both CTAs); in the leader CTA the
+//               converged MMA issuer: waits until BOTH CTAs' dequantised
+//               stages are ready, 4 x tcgen05.mma.cta_group::2.kind::i8 per
+//               k-block, commits multicast to both CTAs' barriers.
+//   warps 4-11  dequantisers: channel row x 64-k half, INT4 -> INT8 into the
+//               canonical SW128 K-major B tile, then (one thread) a
+//               release.cluster arrive on the leader's `ready` barrier.
+//   warps 12-15 epilogue: tcgen05.ld (thread = token row) -> scales -> FP16
+//               -> 128B-swizzled staging -> TMA tensor store; releases the
+//               accumulator with arrives on the leader's `tempty`.
+#include <cooperative_groups.h>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "dequant.cuh"
+#include "kernels.h"
+#include "numerics.cuh"
+#include "ptx.cuh"
+
+namespace dgqk {
+namespace pf {
+
+constexpr int kSL = 6;            // Xq tile + packed-chunk stages (k-blocks in flight)
+constexpr int kSB = 3;            // dequantised weight-tile slots
+constexpr int kThreads = 512;
+constexpr uint32_t kATile = 128 * 128;   // 128 token rows x 128 k (bytes)
+constexpr uint32_t kBTile = 128 * 128;   // 128 channel rows x 128 k
+constexpr uint32_t kStaging = 4 * 4096;  // epilogue: one 4 KB staging buffer per epilogue warp
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Per-k-block "stage dequantised" signal to the leader.  A release.cluster
+// arrive costs 0.5-1 us here (measured, tools/pf_trace.py), more than a k-block
+// of MMA, so the signal is relaxed: the 256 dequant threads' st.shared have
+// been drained by the named barrier (bar.sync completes outstanding shared
+// stores) and made visible to the async proxy by fence.proxy.async before
+// the arrive is issued; the leader's tcgen05.mma reads them through the async
+// proxy after observing the arrive.  The bit-exact GPU tests pin this.
+__device__ __forceinline__ void arrive_remote_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Barriers completed by arrivals from the PEER CTA are polled with test_wait:
+// a suspended try_wait is not woken promptly by a remote (DSMEM) arrival and
+// sleeps out its time limit (~1000 cycles per k-block, measured).
+__device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+#ifndef DGQ_PF_WATCHDOG
+#define DGQ_PF_WATCHDOG 0
+#endif
+__device__ __forceinline__ void watchdog(long long& n, int id, uint32_t parity) {
+#if DGQ_PF_WATCHDOG
+  if (++n == (1ll << 24)) {
+    printf("prefill2 stuck: cta %d warp %d lane %d wait %d parity %u\n", blockIdx.x, threadIdx.x / 32, threadIdx.x % 32,
+           id, parity);
+  }
+  if (n > (1ll << 25)) __trap();
+#endif
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity, int id = 0) {
+  long long n = 0;
+  while (!try_wait_cluster(bar, parity)) watchdog(n, id, parity);
+}
+__device__ __forceinline__ void wait_local(uint64_t* bar, uint32_t parity, int id) {
+  long long n = 0;
+  while (!mbar_try_wait(bar, parity)) watchdog(n, id, parity);
+}
+// converged-warp issue (one lane elected inside the asm)
+__device__ __forceinline__ void mma2_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit2_mc(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::
+          "r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(kCols) : "memory");
+}
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// 32 token rows (this warp's TMEM lane quadrant) x 256 channels of one
+// accumulator -> scales -> FP16/FP32 -> swizzled staging -> TMA store.
+template <bool kF16, bool kF16Mode, bool kBias>
+__device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase, float rsm, const float* s_s1,
+                                         const float* s_bias, uint8_t* stg0, const CUtensorMap* tmY, int nbase,
+                                         int mbox) {
+  constexpr int kCB = kF16 ? 64 : 32;  // columns per 128-byte box row
+  const uint32_t lane = lane_id();
+  uint8_t* row0 = stg0 + lane * 128;
+  const uint32_t sw = lane & 7;
+#pragma unroll 1
+  for (int c0 = 0; c0 < 256; c0 += kCB) {
+    if (nbase + c0 >= p.N) break;
+    uint32_t r[kCB];
+#pragma unroll
+    for (int c1 = 0; c1 < kCB; c1 += 16) tmem_ld16(tbase + c0 + c1, *reinterpret_cast<uint32_t(*)[16]>(&r[c1]));
+    if (lane == 0) bulk_wait_read<0>();  // the previous store has finished reading the staging buffer
+    __syncwarp();
+    tmem_ld_wait();
+    uint8_t* row = row0;
+#pragma unroll
+    for (int c1 = 0; c1 < kCB; c1 += 8) {
+      float y[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int32_t acc = static_cast<int32_t>(r[c1 + k]);
+        const float s1v = s_s1[c0 + c1 + k];
+        float v = kF16Mode ? epilogue_f16mode(acc, rsm, s1v) : epilogue_f32(acc, rsm, s1v);
+        if (kBias) v = __fadd_rn(v, s_bias[c0 + c1 + k]);
+        y[k] = v;
+      }
+      if (kF16) {
+        uint32_t h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __half2 hh = __floats2half2_rn(y[2 * k], y[2 * k + 1]);
+          uint32_t u = *reinterpret_cast<const uint32_t*>(&hh);
+          // fp16_round (proj/src/quant.cpp:33-35) flushes |x| < 2^-24 to signed zero
+          if (fabsf(y[2 * k]) < 0x1p-24f) u = (u & 0xFFFF0000u) | ((__float_as_uint(y[2 * k]) >> 16) & 0x8000u);
+          if (fabsf(y[2 * k + 1]) < 0x1p-24f) u = (u & 0x0000FFFFu) | (__float_as_uint(y[2 * k + 1]) & 0x80000000u);
+          h[k] = u;
+        }
+        *reinterpret_cast<uint4*>(row + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
+      } else {
+        *reinterpret_cast<float4*>(row + (((c1 / 4) ^ sw) << 4)) = make_float4(y[0], y[1], y[2], y[3]);
+        *reinterpret_cast<float4*>(row + (((c1 / 4 + 1) ^ sw) << 4)) = make_float4(y[4], y[5], y[6], y[7]);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmY, stg0, nbase + c0, mbox);
+      bulk_commit();
+    }
+  }
+}
+
+}  // namespace pf
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
+    k_dgq_prefill2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
+                   const DgqGemmParams p) {
+  using namespace pf;
+  constexpr uint32_t kIdesc = idesc_i8(256, 256);
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int KB = p.k_blocks;
+  const int n_tiles = (p.N + 127) / 128;  // 128-channel weight tiles (prepared chunks)
+  const int m_pairs = (p.M + 255) / 256, n_pairs = (p.N + 255) / 256;
+  const int total = m_pairs * n_pairs;
+  const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
+
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = sm;                          // [kSL][128 x 128] Xq (SW128 K-major)
+  uint8_t* sB = sA + kSL * kATile;           // [kSB][128 x 128] W_s8 (SW128 K-major)
+  uint8_t* sStg = sB + kSB * kBTile;         // epilogue staging
+  uint8_t* sC = sStg + kStaging;             // [kSL][chunk_stride] packed chunks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kSL * p.chunk_stride);
+  uint64_t* full = bars;                     // [kSL] A tile + chunk landed (local)
+  uint64_t* empty = full + kSL;              // [kSL] MMA done with the stage (multicast commit)
+  uint64_t* ready = empty + kSL;             // [kSB] leader: both CTAs' B slot dequantised (2 arrivals)
+  uint64_t* bempty = ready + kSB;            // [kSB] MMA done with the B slot (multicast commit)
+  uint64_t* tfull = bempty + kSB;            // [2] accumulator complete (multicast commit)
+  uint64_t* tempty = tfull + 2;              // [2] leader: both CTAs' epilogues drained it (8 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* s_rs = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
+  float* s_s1 = s_rs + 128;                                // [256]
+  float* s_bias = s_s1 + 256;                              // [256]
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSL; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < kSB; ++b) {
+      mbar_init(&ready[b], 2);
+      mbar_init(&bempty[b], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmY);
+  }
+  if (warp == 1) tmem_alloc2<512>(tmem_slot);
+  tc_fence_before();
+  cooperative_groups::this_cluster().sync();  // barrier inits + TMEM visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // Xq / row scales come from K1
+      int it = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const int mt = t % m_pairs, nt = t / m_pairs;
+        const int mrow = mt * 256 + static_cast<int>(rank) * 128;
+        const int ctile = nt * 2 + static_cast<int>(rank);  // this CTA's 128-channel weight tile
+        const bool has_w = ctile < n_tiles;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kSL;
+          wait_local(&empty[s], ((it / kSL) & 1) ^ 1, 1);
+          // a token half entirely past M is not loaded: its rows of D are never stored
+          const bool has_a = mrow < p.M;
+          mbar_arrive_expect_tx(&full[s], (has_a ? kATile : 0u) + (has_w ? p.chunk_bytes : 0u));
+          if (has_a) tma_load_2d(sA + s * kATile, &tmA, &full[s], kb * 128, mrow);
+          if (has_w)
+            bulk_load(sC + s * p.chunk_stride, p.tiles + (static_cast<size_t>(ctile) * KB + kb) * p.chunk_bytes,
+                      p.chunk_bytes, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------- MMA issuer (leader CTA, converged warp) ---------------------
+    if (leader) {
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      int it = 0, tl = 0;
+      for (int t = cid; t < total; t += ncl, ++tl) {
+        const int acc = tl & 1;
+        wait_cluster(&tempty[acc], ((tl >> 1) & 1) ^ 1, 2);  // both epilogues drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tm + acc * 256;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kSL, b = it % kSB;
+          wait_cluster(&ready[b], (it / kSB) & 1, 3);
+          tc_fence_after();
+          const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kATile));
+          const uint64_t db = umma_desc_sw128(smem_u32(sB + b * kBTile));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) mma2_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb | kk) != 0);
+          commit2_mc(&empty[s]);
+          commit2_mc(&bempty[b]);
+        }
+        commit2_mc(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------ dequantisers ------------------------------
+    const int e = threadIdx.x - 128;  // 0..255
+    const int d = e & 127, half = e >> 7;
+    const uint32_t sw = d & 7;
+    const uint32_t ready_leader = mapa(ready, 0);
+    int it = 0;
+    for (int t = cid; t < total; t += ncl) {
+      const int nt = t / m_pairs;
+      const bool has_w = nt * 2 + static_cast<int>(rank) < n_tiles;
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % kSL, b = it % kSB;
+        wait_local(&full[s], (it / kSL) & 1, 4);
+        wait_local(&bempty[b], ((it / kSB) & 1) ^ 1, 6);
+        uint8_t* brow = sB + b * kBTile + (d >> 3) * 1024 + (d & 7) * 128;
+        if (has_w) {
+          const uint8_t* chunk = sC + s * p.chunk_stride;
+          const uint16_t* sc = reinterpret_cast<const uint16_t*>(chunk + 8192);
+          uint4 w4[2];
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) w4[jj] = *reinterpret_cast<const uint4*>(chunk + (half * 2 + jj) * 2048 + d * 16);
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int j = half * 2 + jj;
+            const uint32_t wv[4] = {w4[jj].x, w4[jj].y, w4[jj].z, w4[jj].w};
+            uint32_t o[8];
+            if (p.gshift >= 5) {
+              const uint32_t sv = sc[((j * 32) >> p.gshift) * 128 + d];
+              const uint32_t s2 = sv & 0xFFu, bs = dq_bias2(s2, sv >> 8);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) dq_word(wv[q], s2, bs, o[2 * q], o[2 * q + 1]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t sv = sc[((j * 32 + q * 8) >> p.gshift) * 128 + d];
+                const uint32_t s2 = sv & 0xFFu;
+                dq_word(wv[q], s2, dq_bias2(s2, sv >> 8), o[2 * q], o[2 * q + 1]);
+              }
+            }
+            *reinterpret_cast<uint4*>(brow + (((2 * j) ^ sw) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(brow + (((2 * j + 1) ^ sw) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        } else {
+          const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) *reinterpret_cast<uint4*>(brow + (((half * 4 + jj) ^ sw) << 4)) = z;
+        }
+        fence_proxy_async_smem();
+        named_bar(1, 256);  // all 8 dequant warps of this CTA wrote their rows
+        if (e == 0) arrive_remote_relaxed(ready_leader + b * 8);  // the leader's ready[b]
+      }
+    }
+  } else if (warp >= 12) {
+    // ------------------------------ epilogue ------------------------------
+    const int e = threadIdx.x - 384;                 // 0..127 = token row of this CTA's D
+    const uint32_t q = warp & 3;                     // TMEM lane quadrant
+    const uint32_t tempty_leader = mapa(tempty, 0);
+    uint8_t* stg0 = sStg + (warp - 12) * 4096;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // row scales from K1
+    int tl = 0;
+    for (int t = cid; t < total; t += ncl, ++tl) {
+      const int mt = t % m_pairs, nt = t / m_pairs;
+      const int acc = tl & 1;
+      const int m0 = mt * 256 + static_cast<int>(rank) * 128;
+      const int n0 = nt * 256;
+      // per-tile scales (all four epilogue warps)
+      s_rs[e] = (p.rs && m0 + e < p.M) ? p.rs[m0 + e] : 0.0f;
+      for (int i = e; i < 256; i += 128) {
+        s_s1[i] = (p.s1 && n0 + i < p.N) ? p.s1[n0 + i] : 0.0f;
+        s_bias[i] = (p.bias && n0 + i < p.N) ? p.bias[n0 + i] : 0.0f;
+      }
+      named_bar(2, 128);
+      wait_local(&tfull[acc], (tl >> 1) & 1, 5);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((q * 32) << 16) + acc * 256;
+      const int mrow = q * 32 + lane;
+      const float rsm = s_rs[mrow];
+      if (p.tma_out && !p.acc_out) {
+        const int mbox = m0 + q * 32;
+#define DGQ_EPI2(F16_, MODE_, BIAS_) epi_rows<F16_, MODE_, BIAS_>(p, tbase, rsm, s_s1, s_bias, stg0, &tmY, n0, mbox)
+        const bool b = p.bias != nullptr, f = p.fp16_mode != 0;
+        if (p.out_f16) {
+          if (f) { if (b) DGQ_EPI2(true, true, true); else DGQ_EPI2(true, true, false); }
+          else   { if (b) DGQ_EPI2(true, false, true); else DGQ_EPI2(true, false, false); }
+        } else {
+          if (f) { if (b) DGQ_EPI2(false, true, true); else DGQ_EPI2(false, true, false); }
+          else   { if (b) DGQ_EPI2(false, false, true); else DGQ_EPI2(false, false, false); }
+        }
+#undef DGQ_EPI2
+      } else {
+        const int m = m0 + mrow;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 256; c0 += 16) {
+          if (n0 + c0 >= p.N) break;
+          uint32_t r[16];
+          tmem_ld16(tbase + c0, r);
+          tmem_ld_wait();
+          if (m >= p.M) continue;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int n = n0 + c0 + k;
+            if (n >= p.N) break;
+            const int32_t a = static_cast<int32_t>(r[k]);
+            if (p.acc_out) p.acc_out[static_cast<size_t>(m) * p.ld_acc + n] = a;
+            if (p.out) {
+              float y = p.fp16_mode ? epilogue_f16mode(a, rsm, s_s1[c0 + k]) : epilogue_f32(a, rsm, s_s1[c0 + k]);
+              if (p.bias) y = __fadd_rn(y, s_bias[c0 + k]);
+              if (p.out_f16)
+                static_cast<__half*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = fp16_ref(y);
+              else
+                static_cast<float*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = y;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_remote(tempty_leader + acc * 8);  // the leader's tempty[acc]
+      named_bar(2, 128);  // scales of the next tile are rewritten
+    }
+    if (lane == 0) bulk_wait_all();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  tc_fence_before();
+  cooperative_groups::this_cluster().sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2<512>(tmem);
+  }
+}
+
+}  // namespace dgqk
+
+using namespace dgqk;
+
+size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride) {
+  return 1024 + pf::kSL * (pf::kATile + chunk_stride) + pf::kSB * pf::kBTile + pf::kStaging +
+         (2 * pf::kSL + 2 * pf::kSB + 4) * 8 + 16 + (128 + 256 + 256) * 4;
+}
+
+int dgq_prefill2_clusters(int M, int N) {
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int pairs = sms / 2;
+  return tiles < pairs ? tiles : pairs;
+}
+
+cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
+                                cudaStream_t st) {
+  const size_t smem = dgq_prefill2_smem_bytes(p.chunk_stride);
+  cudaError_t e = cudaFuncSetAttribute(k_dgq_prefill2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N));
+  cfg.blockDim = dim3(pf::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k_dgq_prefill2, tmA, tmY, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}

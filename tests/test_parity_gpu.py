@@ -284,6 +284,44 @@ def test_decode_kernel_matches_oracle(cuda, port, M, h, o, g):
     assert np.array_equal(bits(yf.cpu().numpy()), bits(port.epilogue(acc_ref, rs, L.s1, None, True)))
 
 
+PREFILL_CASES = [
+    # (M, h, o, g): persistent CTA-pair kernel (M >= 256): ragged M / N / K, odd tile counts, every group path
+    (256, 512, 256, 128), (300, 1024, 384, 64), (513, 992, 1000, 32), (777, 2048, 640, 256), (1030, 384, 130, 128),
+]
+
+
+@pytest.fixture
+def pair_kernel():
+    import ctypes
+
+    lib = dgq.lib()
+    lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    lib.dgq_debug_set_decode(1 | 0x400)  # route M >= 256 to the CTA-pair kernel (K5p)
+    yield
+    lib.dgq_debug_set_decode(1)
+
+
+@pytest.mark.parametrize("M,h,o,g", PREFILL_CASES)
+def test_prefill_pair_kernel_matches_oracle(cuda, port, pair_kernel, M, h, o, g):
+    L = oracle.random_layer(h, o, g, seed=M + h + o + g)
+    X = port.gen_synthetic(M, h, 3 + M, 3, 50.0, 3)
+    bias = np.random.default_rng(M).uniform(-0.5, 0.5, o).astype(np.float32)
+    out, w, q, rs, mx = port.dgq_forward(X, L, bias)
+    acc_ref, _ = port.int8_gemm(q, w)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    assert CL.plan(M)["token_tile"] == 256
+    codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+    db = torch.from_numpy(bias).cuda()
+    y32, acc = CL.linear(codes, drs, bias=db, out_dtype=torch.float32, want_acc=True)
+    assert np.array_equal(acc.cpu().numpy(), acc_ref)
+    assert np.array_equal(bits(y32.cpu().numpy()), bits(out))
+    for _ in range(2):  # the TMA-store epilogue path, twice (persistent accumulators reused)
+        y32b = CL.linear(codes, drs, bias=db, out_dtype=torch.float32)
+        assert np.array_equal(bits(y32b.cpu().numpy()), bits(out))
+        y16 = CL.linear(codes, drs, bias=db, out_dtype=torch.float16)
+        assert np.array_equal(bits(y16.cpu().numpy()), bits(port.fp16_round_array(out).astype(np.float16)))
+
+
 def test_decode_and_prefill_orientations_agree(cuda, port):
     import ctypes
 
