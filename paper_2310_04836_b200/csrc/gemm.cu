@@ -569,8 +569,13 @@ extern "C" int dgq_debug_decode_mode() { return g_decode_mode; }
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn, int force_splits) {
   DgqGemmPlan pl{};
   const int kblocks = K_pad / 128;
-  // K5p is opt-in (tools / tests: mode bit 10) until it beats the one-CTA kernel below
-  if (fused && M >= 256 && (g_decode_mode & 0x400) != 0 && !force_bn && !force_splits &&
+  // K5p (CTA pairs) wins when its 256 x 256 pair tiles fill >= 6 waves of the
+  // SM pairs (e.g. OPT-30B fc1 at 2048 tokens: 2569 vs 2443 TOPS); with fewer
+  // tiles the last wave's imbalance costs more than the pair saves, and the
+  // one-CTA kernel below is used (tools / tests: mode bit 10 forces K5p).
+  const long long pair_tiles = static_cast<long long>((M + 255) / 256) * ((N + 255) / 256);
+  const bool pair_ok = (g_decode_mode & 0x400) != 0 || pair_tiles >= 6LL * (sm_count() / 2);
+  if (fused && M >= 256 && pair_ok && !force_bn && !force_splits &&
       dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128))) <= 232448) {
     // K5p: persistent CTA pairs
     pl.prefill2 = 1;

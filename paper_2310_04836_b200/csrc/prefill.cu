@@ -42,9 +42,11 @@
 namespace dgqk {
 namespace pf {
 
-constexpr int kSL = 6;            // Xq tile + packed-chunk stages (k-blocks in flight)
-constexpr int kSB = 3;            // dequantised weight-tile slots
-constexpr int kThreads = 512;
+constexpr int kSL = 5;            // Xq tile + packed-chunk stages (k-blocks in flight)
+constexpr int kSB = 4;            // dequantised weight-tile slots (> dequant groups: a group can run ahead)
+constexpr int kDqGroups = 3;      // groups of four dequant warps, alternate k-blocks
+constexpr int kEpiWarp0 = 4 + 4 * kDqGroups;  // first of the four epilogue warps
+constexpr int kThreads = 32 * (kEpiWarp0 + 4);
 constexpr uint32_t kATile = 128 * 128;   // 128 token rows x 128 k (bytes)
 constexpr uint32_t kBTile = 128 * 128;   // 128 channel rows x 128 k
 constexpr uint32_t kStaging = 4 * 4096;  // epilogue: one 4 KB staging buffer per epilogue warp
@@ -301,6 +303,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % kSL, b = it % kSB;
           wait_cluster(&ready[b], (it / kSB) & 1, 3);
+          if (p.dbg && blockIdx.x == 0 && lane == 0 && it < 1024) {  // tools/pf_trace.py
+            uint64_t g;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+            p.dbg[it] = g;
+          }
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kATile));
           const uint64_t db = umma_desc_sw128(smem_u32(sB + b * kBTile));
@@ -313,10 +320,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= 4 && warp < static_cast<uint32_t>(kEpiWarp0)) {
     // ------------------------------ dequantisers ------------------------------
-    const int e = threadIdx.x - 128;  // 0..255
-    const int d = e & 127, half = e >> 7;
+    // kDqGroups groups of four warps take k-blocks round robin, so several
+    // k-blocks are in flight: one k-block's dequantisation is latency-bound
+    // (~1700 cycles for 128 rows on four SMSPs, tools/pf_trace.py), well above
+    // the 512-cycle MMA step it feeds.
+    const int grp = (warp - 4) >> 2;
+    const int d = static_cast<int>((warp & 3) * 32 + lane);  // channel row of this CTA's B tile
     const uint32_t sw = d & 7;
     const uint32_t ready_leader = mapa(ready, 0);
     int it = 0;
@@ -324,6 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       const int nt = t / m_pairs;
       const bool has_w = nt * 2 + static_cast<int>(rank) < n_tiles;
       for (int kb = 0; kb < KB; ++kb, ++it) {
+        if (it % kDqGroups != grp) continue;
         const int s = it % kSL, b = it % kSB;
         wait_local(&full[s], (it / kSL) & 1, 4);
         wait_local(&bempty[b], ((it / kSB) & 1) ^ 1, 6);
@@ -331,13 +343,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         if (has_w) {
           const uint8_t* chunk = sC + s * p.chunk_stride;
           const uint16_t* sc = reinterpret_cast<const uint16_t*>(chunk + 8192);
-          uint4 w4[2];
+          uint4 w4[4];
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) w4[jj] = *reinterpret_cast<const uint4*>(chunk + (half * 2 + jj) * 2048 + d * 16);
+          for (int j = 0; j < 4; ++j) w4[j] = *reinterpret_cast<const uint4*>(chunk + j * 2048 + d * 16);
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const int j = half * 2 + jj;
-            const uint32_t wv[4] = {w4[jj].x, w4[jj].y, w4[jj].z, w4[jj].w};
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t wv[4] = {w4[j].x, w4[j].y, w4[j].z, w4[j].w};
             uint32_t o[8];
             if (p.gshift >= 5) {
               const uint32_t sv = sc[((j * 32) >> p.gshift) * 128 + d];
@@ -358,19 +369,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         } else {
           const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) *reinterpret_cast<uint4*>(brow + (((half * 4 + jj) ^ sw) << 4)) = z;
+          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(brow + ((c ^ sw) << 4)) = z;
         }
         fence_proxy_async_smem();
-        named_bar(1, 256);  // all 8 dequant warps of this CTA wrote their rows
-        if (e == 0) arrive_remote_relaxed(ready_leader + b * 8);  // the leader's ready[b]
+        named_bar(3 + grp, 128);  // the group's four warps wrote their rows (barrier ids 3..)
+        if (d == 0) arrive_remote_relaxed(ready_leader + b * 8);  // the leader's ready[b]
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= static_cast<uint32_t>(kEpiWarp0)) {
     // ------------------------------ epilogue ------------------------------
-    const int e = threadIdx.x - 384;                 // 0..127 = token row of this CTA's D
+    const int e = threadIdx.x - 32 * kEpiWarp0;      // 0..127 = token row of this CTA's D
     const uint32_t q = warp & 3;                     // TMEM lane quadrant
     const uint32_t tempty_leader = mapa(tempty, 0);
-    uint8_t* stg0 = sStg + (warp - 12) * 4096;
+    uint8_t* stg0 = sStg + (warp - kEpiWarp0) * 4096;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // row scales from K1
     int tl = 0;
     for (int t = cid; t < total; t += ncl, ++tl) {

@@ -9,7 +9,14 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2310_04836_b200 as dgq  # noqa: E402
 
-Ms = [int(v) for v in sys.argv[1:]] or [1, 16, 64, 512, 2048]
+import ctypes  # noqa: E402
+
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+if "--pair" in sys.argv:  # route M >= 256 to the CTA-pair prefill kernel (K5p)
+    _l = dgq.lib()
+    _l.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    _l.dgq_debug_set_decode(1 | 0x400)
+Ms = [int(v) for v in args] or [1, 16, 64, 512, 2048]
 shapes = [("q 7168x7168", 7168, 7168), ("fc1 7168x28672", 7168, 28672), ("fc2 28672x7168", 28672, 7168),
           ("llama7b up 4096x11008", 4096, 11008), ("c1 4096x4096", 4096, 4096)]
 g = 128

@@ -1,5 +1,5 @@
-"""K5p (prefill pair kernel) per-k-block cycle counts of CTA 0 (leader):
-MMA wait for `ready`, dequant wait for `full`, dequant work.  python tools/pf_trace.py M K N"""
+"""K5p per-k-block timeline of the first CTA pair (globaltimer, us): when the
+leader's MMA issuer observes each k-block ready, and the median period.  python tools/pf_trace.py M K N"""
 import ctypes as C
 import os
 import sys
@@ -16,36 +16,26 @@ CL = dgq.CudaLayer(L, validate=False)
 x = torch.randn(M, K, device="cuda") * 3
 codes, rs = CL.quantize_act(x)
 out = torch.empty(M, N, dtype=torch.float16, device="cuda")
-buf = torch.zeros(7 * 2048, dtype=torch.int64, device="cuda")
+buf = torch.zeros(9 * 1024, dtype=torch.int64, device="cuda")
 lib = dgq.lib()
 lib.dgq_debug_set_timestamps.argtypes = [C.c_void_p]
+lib.dgq_debug_set_decode.argtypes = [C.c_int]
+lib.dgq_debug_set_decode(1 | 0x400)
 for _ in range(2):
     CL.linear(codes, rs, out=out)
 torch.cuda.synchronize()
 lib.dgq_debug_set_timestamps(C.c_void_p(buf.data_ptr()))
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
 CL.linear(codes, rs, out=out)
-e1.record()
 torch.cuda.synchronize()
 lib.dgq_debug_set_timestamps(None)
-t = e0.elapsed_time(e1) * 1e3
-print(f"{t:.1f} us  {2 * M * N * K / t / 1e6:.0f} TOPS")
-bb = buf.cpu().numpy()
-a0, a1, mo = bb[6144:6144 + 1024], bb[7168:8192], bb[8192:9216]
-nn = int((mo > 0).sum())
-t0 = min(a0[a0 > 0].min(), a1[a1 > 0].min(), mo[mo > 0].min())
-ws, wf = bb[2048:3072], bb[3072:4096]
-print("k-block: leader deq start / data ready / arrive | peer arrive | mma sees ready (us)")
-for i in list(range(0, 8)) + list(range(40, 48)):
-    print(f"  {i:4d}: {(ws[i] - t0) / 1e3:8.3f} {(wf[i] - t0) / 1e3:8.3f} {(a0[i] - t0) / 1e3:8.3f} | "
-          f"{(a1[i] - t0) / 1e3:8.3f} | {(mo[i] - t0) / 1e3:8.3f}")
-pe0, pe1 = bb[9216:10240], bb[10240:11264]
-print("producer empty-wait cycles leader:", pe0[:12].tolist(), " median", np.median(pe0[4:nn]))
-print("producer empty-wait cycles peer:  ", pe1[:12].tolist(), " median", np.median(pe1[4:nn]))
-print("arrive_remote ns leader:", bb[11264:11264 + 12].tolist(), " peer:", bb[12288:12288 + 12].tolist())
-b = bb[:3 * 2048].reshape(3, 2048)
+b = buf.view(9, 1024).cpu().numpy()
+t0 = b[b > 0].min()
+r = lambda v: (v - t0) / 1e3  # noqa: E731
+print(" kb | lead: start  slot-ok  arrive | peer: start  slot-ok  arrive | mma ready")
+for i in list(range(0, 6)) + list(range(60, 69)):
+    print(f"{i:3d} | {r(b[3][i]):6.2f} {r(b[5][i]):6.2f} {r(b[1][i]):6.2f} | {r(b[4][i]):6.2f} {r(b[6][i]):6.2f} "
+          f"{r(b[2][i]):6.2f} | {r(b[0][i]):6.2f}")
 n = int((b[0] > 0).sum())
-for name, r in (("mma wait ready", 0), ("deq wait full", 1), ("deq work", 2)):
-    v = b[r][:n]
-    print(f"{name:15s} median {np.median(v):7.0f}  mean {v.mean():7.0f}  first {v[:8].tolist()}")
+d = np.diff(b[0][:n]) / 1e3
+print(f"MMA period median {np.median(d):.3f} us over {n} k-blocks")
+lib.dgq_debug_set_decode(1)
