@@ -259,8 +259,15 @@ class OptLayer:
         x = self.x[:M]
         self._k1("q", x, M)
         cq, rq = self.codes["q"], self.rs["q"]
-        for n in ("q", "k", "v"):
-            self._k5(n, cq, rq, M)
+        if M <= 32:
+            # decode: q / k / v share the input -> one K5d launch over the three weight sets
+            from paper_2310_04836_b200 import linear_multi
+
+            linear_multi([self.lin[n].layer for n in ("q", "k", "v")], cq[:M], rq[:M],
+                         outs=[self.y[n][:M] for n in ("q", "k", "v")])
+        else:
+            for n in ("q", "k", "v"):
+                self._k5(n, cq, rq, M)
         a = self._gather("q", M)  # attention-output stand-in, gathered for the out projection
         self._k1("out", a, M)
         self._k5("out", self.codes["out"], self.rs["out"], M)

@@ -131,6 +131,17 @@ dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx,
 dgq_status dgq_linear(const dgq_layer* layer, const int8_t* dXq, size_t ldq, const float* dRowScale, size_t M,
                       const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
                       size_t ld_acc, void* dWorkspace, size_t ws_bytes, void* stream);
+/* Several layers that share the input (q / k / v of a decoder layer, gate / up
+ * of an MLP): `count` (1..4) outputs from one activation-code buffer.  Decode-
+ * shaped calls (M <= 32) run as ONE K5d launch over the concatenation of the
+ * layers' weight tiles (one stream-K problem: fewer launches, better balance);
+ * other shapes fall back to one dgq_linear per layer.  Layers must share h, g.
+ * dBias may be NULL or hold NULL entries; dY[i] is [M x ldy[i]].  dWorkspace:
+ * dgq_linear_multi_workspace_bytes zeroed bytes, or NULL for layers[0]'s own. */
+dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int8_t* dXq, size_t ldq,
+                            const float* dRowScale, size_t M, const float* const* dBias, int out_dtype,
+                            void* const* dY, const size_t* ldy, void* dWorkspace, size_t ws_bytes, void* stream);
+size_t dgq_linear_multi_workspace_bytes(const dgq_layer* const* layers, int count, size_t M);
 /* K1 + K5 in one call; dXq [M x k_pad] and dRowScale [M] are caller scratch. */
 dgq_status dgq_forward_device(const dgq_layer* layer, const float* dX, size_t M, size_t ldx, const float* dBias,
                               int out_dtype, void* dY, size_t ldy, int8_t* dXq, float* dRowScale, void* dWorkspace,

@@ -79,6 +79,9 @@ _SIGS = {
     "dgq_int8_gemm": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, _vp, _sz, C.POINTER(C.c_int64), _vp]),
     "dgq_epilogue": (_i, [_vp, _sz, _vp, _vp, _vp, _sz, _sz, _i, _i, _vp, _sz, _vp]),
     "dgq_audit_max_abs_acc": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, C.POINTER(C.c_int64), _vp]),
+    "dgq_linear_multi": (_i, [C.POINTER(_vp), _i, _vp, _sz, _vp, _sz, C.POINTER(_vp), _i, C.POINTER(_vp),
+                              C.POINTER(_sz), _vp, _sz, _vp]),
+    "dgq_linear_multi_workspace_bytes": (_sz, [C.POINTER(_vp), _i, _sz]),
     # host-buffer API (the reference's calling convention)
     "dgq_host_quantize_activations": (_i, [_vp, _sz, _sz, _vp, _i, _f, _vp, _vp]),
     "dgq_host_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp]),

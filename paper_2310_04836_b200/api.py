@@ -270,6 +270,23 @@ class CudaLayer:
 # Reference-API mirror (proj/include/dgq/kernel.hpp:15-53), host in / host out
 # ---------------------------------------------------------------------------
 
+def linear_multi(layers, codes: torch.Tensor, rs: torch.Tensor, outs=None, biases=None, out_dtype=torch.float16):
+    """Several CudaLayers that share the input (q/k/v): one K5d launch over all of
+    their weight tiles for decode-shaped M (dgq_linear_multi); returns the outputs."""
+    n = len(layers)
+    M = codes.shape[0]
+    if outs is None:
+        outs = [torch.empty(M, L.o, dtype=out_dtype, device=codes.device) for L in layers]
+    hs = (C.c_void_p * n)(*[L.handle for L in layers])
+    ys = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    lds = (C.c_size_t * n)(*[o.stride(0) for o in outs])
+    bs = None if biases is None else (C.c_void_p * n)(*[None if b is None else b.data_ptr() for b in biases])
+    od = OUT_F16 if outs[0].dtype == torch.float16 else OUT_F32
+    check(lib().dgq_linear_multi(hs, n, _t_ptr(codes), codes.stride(0), _t_ptr(rs), M, bs, od, ys, lds, None, 0,
+                                 _stream(codes.device)))
+    return outs
+
+
 @dataclass
 class ActQuant:
     codes: np.ndarray        # int8 [b x h]

@@ -486,6 +486,69 @@ dgq_status dgq_quantize_act(const dgq_layer* L, const float* dX, size_t M, size_
   return DGQ_OK;
 }
 
+struct DecodeSub {
+  const uint8_t* tiles;
+  const float* s1;
+  const float* bias;
+  void* out;
+  size_t ldy;
+  int N;
+};
+
+// K5d over `count` layers that share the input (one stream-K problem over the
+// concatenation of their weight tiles).  ws: dgq_decode_workspace(total tiles).
+static dgq_status run_decode(const DecodeSub* subs, int count, int g, size_t k_pad, const int8_t* dXq, size_t ldq,
+                             size_t M, const float* dRs, int out_dtype, int fp16_mode, int32_t* dAcc, size_t ld_acc,
+                             void* ws, cudaStream_t st) {
+  int total_tiles = 0;
+  for (int i = 0; i < count; ++i) total_tiles += (subs[i].N + 127) / 128;
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), total_tiles * 128, static_cast<int>(k_pad), true, g);
+  if (!pl.decode) return fail(DGQ_EINVAL, "not a decode-shaped call");
+  DgqDecodeParams d{};
+  d.nsub = count;
+  int tb = 0;
+  for (int i = 0; i < count; ++i) {
+    d.sub[i] = DgqDecodeSub{subs[i].tiles, subs[i].s1, subs[i].bias, subs[i].out, subs[i].ldy, subs[i].N, tb};
+    tb += (subs[i].N + 127) / 128;
+  }
+  d.chunk_bytes = static_cast<uint32_t>(dgq_layout::chunk_bytes(g));
+  d.chunk_stride = d.chunk_bytes;
+  d.gpk = g >= 128 ? 1 : 128 / g;
+  d.gshift = 7;
+  if (g < 128) {
+    d.gshift = 0;
+    while ((1 << d.gshift) < g) ++d.gshift;
+  }
+  {
+    // units per stage: as many as the TMEM partial ring allows with >= 2 slots
+    const int per = d.gpk * pl.bn;
+    const int ku = 128 / per;
+    const int ups = dgq_decode_units_per_stage(pl.bn);
+    d.ku = ku < 1 ? 1 : (ku > ups ? ups : ku);
+    const int room = 256 / (d.ku * per);  // TMEM columns [256, 512) hold the partial ring
+    d.sd_log2 = room >= 8 ? 3 : (room >= 4 ? 2 : (room >= 2 ? 1 : 0));
+  }
+  CUtensorMap tmB;
+  dgq_status ms =
+      make_tmap_kblocks(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn), static_cast<uint32_t>(d.ku));
+  if (ms != DGQ_OK) return ms;
+  d.M = static_cast<int>(M);
+  d.n_tiles = total_tiles;
+  d.k_blocks = static_cast<int>(k_pad / 128);
+  d.rs = dRs;
+  d.out_f16 = out_dtype == DGQ_OUT_F16;
+  d.fp16_mode = fp16_mode;
+  d.acc_out = count == 1 ? dAcc : nullptr;
+  d.ld_acc = ld_acc;
+  d.ws = static_cast<int32_t*>(ws);
+  d.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
+  d.dbg = (dgq_debug_decode_mode() >> 1) & 0x7F;
+  d.trace = g_dbg_ts;
+  d.trace_cta = 0;
+  DGQ_CUDA(dgq_launch_decode(pl.bn, tmB, d, pl.ctas, pl.pdl != 0, st));
+  return DGQ_OK;
+}
+
 static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& tmA, int g, size_t N, size_t k_pad,
                            const int8_t* dXq, size_t ldq, size_t M, const float* dRs, const float* dS1,
                            const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
@@ -497,48 +560,9 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
   dgq_status ms = make_tmap(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn));
   if (ms != DGQ_OK) return ms;
   if (pl.decode) {
-    DgqDecodeParams d{};
-    d.tiles = tiles;
-    d.chunk_bytes = static_cast<uint32_t>(dgq_layout::chunk_bytes(g));
-    d.chunk_stride = d.chunk_bytes;
-    d.gpk = g >= 128 ? 1 : 128 / g;
-    d.gshift = 7;
-    if (g < 128) {
-      d.gshift = 0;
-      while ((1 << d.gshift) < g) ++d.gshift;
-    }
-    {
-      // units per stage: as many as the TMEM partial ring allows with >= 2 slots
-      const int per = d.gpk * pl.bn;
-      int ku = 128 / per;
-      const int ups = dgq_decode_units_per_stage(pl.bn);
-      d.ku = ku < 1 ? 1 : (ku > ups ? ups : ku);
-      const int room = 256 / (d.ku * per);  // TMEM columns [256, 512) hold the partial ring
-      d.sd_log2 = room >= 8 ? 3 : (room >= 4 ? 2 : (room >= 2 ? 1 : 0));
-    }
-    ms = make_tmap_kblocks(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn), static_cast<uint32_t>(d.ku));
-    if (ms != DGQ_OK) return ms;
-    d.M = static_cast<int>(M);
-    d.N = static_cast<int>(N);
-    d.n_tiles = pl.n_tiles;
-    d.k_blocks = static_cast<int>(k_pad / 128);
-    d.rs = dRs;
-    d.s1 = dS1;
-    d.bias = dBias;
-    d.out = dY;
-    d.ldy = ldy;
-    d.out_f16 = out_dtype == DGQ_OUT_F16;
-    d.fp16_mode = fp16_mode;
-    d.acc_out = dAcc;
-    d.ld_acc = ld_acc;
-    d.ws = static_cast<int32_t*>(ws);
-    d.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
     if (!ws) return fail(DGQ_EINVAL, "decode kernel needs a workspace");
-    d.dbg = (dgq_debug_decode_mode() >> 1) & 0x7F;
-    d.trace = g_dbg_ts;
-    d.trace_cta = 0;
-    DGQ_CUDA(dgq_launch_decode(pl.bn, tmB, d, pl.ctas, pl.pdl != 0, st));
-    return DGQ_OK;
+    DecodeSub one{tiles, dS1, dBias, dY, ldy, static_cast<int>(N)};
+    return run_decode(&one, 1, g, k_pad, dXq, ldq, M, dRs, out_dtype, fp16_mode, dAcc, ld_acc, ws, st);
   }
   DgqGemmParams p{};
   p.tiles = tiles;
@@ -748,6 +772,68 @@ dgq_status dgq_epilogue(const int32_t* dAcc, size_t lda, const float* dRs, const
   DGQ_CUDA(dgq_launch_epilogue(dAcc, lda, dRs, dS1, dBias, static_cast<int>(M), static_cast<int>(N), fp16_mode,
                                out_dtype == DGQ_OUT_F16, dY, ldy, static_cast<cudaStream_t>(stream)));
   return DGQ_OK;
+}
+
+dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int8_t* dXq, size_t ldq,
+                            const float* dRowScale, size_t M, const float* const* dBias, int out_dtype,
+                            void* const* dY, const size_t* ldy, void* dWorkspace, size_t ws_bytes, void* stream) {
+  if (!layers || count < 1 || count > kDecodeMaxSub || !dY || !ldy)
+    return fail(DGQ_EINVAL, "dgq_linear_multi: 1..4 layers with outputs");
+  const dgq_layer* L0 = layers[0];
+  for (int i = 0; i < count; ++i) {
+    if (!layers[i] || !dY[i]) return fail(DGQ_EINVAL, "null layer or output");
+    if (layers[i]->h != L0->h || layers[i]->g != L0->g || layers[i]->fused != L0->fused)
+      return fail(DGQ_EINVAL, "dgq_linear_multi: layers must share h, g and the prepared layout");
+  }
+  if (M == 0) return DGQ_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int total_tiles = 0;
+  for (int i = 0; i < count; ++i) total_tiles += layers[i]->n_tiles;
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), total_tiles * 128, static_cast<int>(L0->k_pad), L0->fused,
+                                 static_cast<int>(L0->g));
+  if (!pl.decode) {  // not decode-shaped: one launch per layer
+    for (int i = 0; i < count; ++i) {
+      dgq_status s = dgq_linear(layers[i], dXq, ldq, dRowScale, M, dBias ? dBias[i] : nullptr, out_dtype, 0, dY[i],
+                                ldy[i], nullptr, 0, nullptr, 0, stream);
+      if (s != DGQ_OK) return s;
+    }
+    return DGQ_OK;
+  }
+  if (ldq != L0->k_pad) return fail(DGQ_EINVAL, "ldq must equal the layers' k_pad");
+  if (!dXq || !dRowScale) return fail(DGQ_EINVAL, "null activation codes or row scales");
+  const size_t need = pl.ws_bytes + pl.counter_bytes;
+  void* ws = dWorkspace;
+  auto* L = const_cast<dgq_layer*>(L0);
+  std::unique_lock<std::mutex> lk(L->ws_mu, std::defer_lock);
+  if (!ws) {  // the first layer's internal workspace, grown to the combined problem
+    lk.lock();
+    if (L->ws_cap < need) {
+      cudaFree(L->ws);
+      L->ws = nullptr;
+      L->ws_cap = 0;
+      DGQ_CUDA(cudaMalloc(&L->ws, need));
+      DGQ_CUDA(cudaMemset(L->ws, 0, need));
+      L->ws_cap = need;
+    }
+    ws = L->ws;
+  } else if (ws_bytes < need) {
+    return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(need));
+  }
+  DecodeSub subs[kDecodeMaxSub];
+  for (int i = 0; i < count; ++i)
+    subs[i] = DecodeSub{layers[i]->tiles, layers[i]->s1, dBias ? dBias[i] : nullptr, dY[i], ldy[i],
+                        static_cast<int>(layers[i]->o)};
+  return run_decode(subs, count, static_cast<int>(L0->g), L0->k_pad, dXq, ldq, M, dRowScale, out_dtype, 0, nullptr, 0,
+                    ws, st);
+}
+
+size_t dgq_linear_multi_workspace_bytes(const dgq_layer* const* layers, int count, size_t M) {
+  if (!layers || count < 1 || M == 0) return 0;
+  int total_tiles = 0;
+  for (int i = 0; i < count; ++i) total_tiles += layers[i] ? layers[i]->n_tiles : 0;
+  DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), total_tiles * 128, static_cast<int>(layers[0]->k_pad),
+                                 layers[0]->fused, static_cast<int>(layers[0]->g));
+  return pl.ws_bytes + pl.counter_bytes;
 }
 
 }  // extern "C"

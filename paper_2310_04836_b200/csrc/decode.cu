@@ -111,24 +111,40 @@ struct StageWalk {
 };
 
 template <int BN>
-__device__ __forceinline__ void store_final(const DgqDecodeParams& p, int n, const int32_t (&acc)[BN]) {
-  if (n >= p.N) return;
-  const float s1v = p.s1 ? p.s1[n] : 0.0f;
-  const float bv = p.bias ? p.bias[n] : 0.0f;
+__device__ __forceinline__ void store_final(const DgqDecodeParams& p, int t, int e, const int32_t (&acc)[BN]) {
+  int li = 0;  // which layer the global tile t belongs to
+#pragma unroll
+  for (int i = 1; i < kDecodeMaxSub; ++i)
+    if (i < p.nsub && t >= p.sub[i].tile_begin) li = i;
+  const DgqDecodeSub& sb = p.sub[li];
+  const int n = (t - sb.tile_begin) * 128 + e;
+  if (n >= sb.N) return;
+  const float s1v = sb.s1 ? sb.s1[n] : 0.0f;
+  const float bv = sb.bias ? sb.bias[n] : 0.0f;
 #pragma unroll
   for (int m = 0; m < BN; ++m) {
     if (m >= p.M) break;
     if (p.acc_out) p.acc_out[static_cast<size_t>(m) * p.ld_acc + n] = acc[m];
-    if (p.out) {
+    if (sb.out) {
       const float rsm = p.rs[m];
       float y = p.fp16_mode ? epilogue_f16mode(acc[m], rsm, s1v) : epilogue_f32(acc[m], rsm, s1v);
-      if (p.bias) y = __fadd_rn(y, bv);
+      if (sb.bias) y = __fadd_rn(y, bv);
       if (p.out_f16)
-        static_cast<__half*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = fp16_ref(y);
+        static_cast<__half*>(sb.out)[static_cast<size_t>(m) * sb.ldy + n] = fp16_ref(y);
       else
-        static_cast<float*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = y;
+        static_cast<float*>(sb.out)[static_cast<size_t>(m) * sb.ldy + n] = y;
     }
   }
+}
+
+// global address of the prepared chunk of (global tile t, k-block kb)
+__device__ __forceinline__ const uint8_t* chunk_addr(const DgqDecodeParams& p, int t, int kb) {
+  int li = 0;
+#pragma unroll
+  for (int i = 1; i < kDecodeMaxSub; ++i)
+    if (i < p.nsub && t >= p.sub[i].tile_begin) li = i;
+  return p.sub[li].tiles +
+         (static_cast<size_t>(t - p.sub[li].tile_begin) * p.k_blocks + kb) * static_cast<size_t>(p.chunk_bytes);
 }
 
 }  // namespace dec
@@ -204,8 +220,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
         if (weights) {
           mbar_wait(&empty[sl], ((w.idx / SL) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[sl], w.cnt * p.chunk_bytes + ku * kBBytes);
-          bulk_load(sC + sl * stage_cb, p.tiles + (u0 + (nu - w.left)) * static_cast<long long>(p.chunk_bytes),
-                    w.cnt * p.chunk_bytes, &full[sl]);
+          bulk_load(sC + sl * stage_cb, dec::chunk_addr(p, w.tile, w.kb), w.cnt * p.chunk_bytes, &full[sl]);
           dec::trace_stamp(p, 0, w.idx);
         }
         if (btile) tma_load_3d(sB + sl * UPS * kBBytes, &tmB, &full[sl], 0, 0, w.kb);
@@ -373,9 +388,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
       if (w.ends_segment(KB)) {
         const int t = w.tile;
         const long long tb = static_cast<long long>(t) * KB, te = tb + KB;
-        const int n = t * 128 + e;
         if (seg_from_tile_start && w.kb + w.cnt == KB) {
-          dec::store_final<BN>(p, n, acc);
+          dec::store_final<BN>(p, t, e, acc);
         } else {
           int32_t* ws = p.ws + static_cast<size_t>(t) * BN * 128 + e;
 #pragma unroll
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
                 ws[m * 128] = 0;
               }
             }
-            dec::store_final<BN>(p, n, acc);
+            dec::store_final<BN>(p, t, e, acc);
             if (e == 0) p.counters[t] = 0u;
           }
           named_bar(2, 128);  // s_flag is rewritten by the next segment

@@ -59,9 +59,23 @@ struct DgqGemmParams {
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
 };
 
-// K5d (decode.cu): stream-K over (weight tile, k-block) units, raw codes as
-// the unsigned A operand from TMEM, group scales applied to TMEM partials.
+// K5d (decode.cu): stream-K over (weight tile, k-block) units, (code - ZP) as
+// the signed A operand from TMEM, group scales applied to TMEM partials.
+// Up to kDecodeMaxSub layers that share the input (e.g. q / k / v) form ONE
+// stream-K problem over the concatenation of their weight tiles.
+constexpr int kDecodeMaxSub = 4;
+struct DgqDecodeSub {
+  const uint8_t* tiles;
+  const float* s1;
+  const float* bias;
+  void* out;
+  size_t ldy;
+  int N;
+  int tile_begin;  // first global tile of this layer
+};
 struct DgqDecodeParams {
+  int nsub;  // number of layers (1 = the single-layer fields below are mirrored in sub[0])
+  DgqDecodeSub sub[kDecodeMaxSub];
   const uint8_t* tiles;
   uint32_t chunk_bytes;
   uint32_t chunk_stride;

@@ -322,6 +322,27 @@ def test_prefill_pair_kernel_matches_oracle(cuda, port, pair_kernel, M, h, o, g)
         assert np.array_equal(bits(y16.cpu().numpy()), bits(port.fp16_round_array(out).astype(np.float16)))
 
 
+@pytest.mark.parametrize("M", [1, 13, 32, 40])
+def test_linear_multi_shared_input(cuda, port, M):
+    # q / k / v style: three layers over one input, one K5d launch for M <= 32
+    # (per-layer launches above); must equal the three separate linears bit for bit
+    h, g = 1024, 128
+    Ls = [oracle.random_layer(h, o, g, seed=o) for o in (256, 384, 130)]
+    for L in Ls[1:]:
+        L.k = Ls[0].k  # shared input => shared smoothing vector
+    X = port.gen_synthetic(M, h, 11, 3, 50.0, 3)
+    CLs = [dgq.CudaLayer(_to_dgq(L)) for L in Ls]
+    codes, drs = CLs[0].quantize_act(torch.from_numpy(X).cuda())
+    biases = [None, torch.from_numpy(np.linspace(-1, 1, 384).astype(np.float32)).cuda(), None]
+    outs = dgq.linear_multi(CLs, codes, drs, biases=biases, out_dtype=torch.float32)
+    for i, (L, CL) in enumerate(zip(Ls, CLs)):
+        ref, *_ = port.dgq_forward(X, L, None if biases[i] is None else biases[i].cpu().numpy())
+        assert np.array_equal(bits(outs[i].cpu().numpy()), bits(ref)), i
+    outs2 = dgq.linear_multi(CLs, codes, drs, biases=biases, out_dtype=torch.float32)  # workspace left zeroed
+    for a, b in zip(outs, outs2):
+        assert np.array_equal(bits(a.cpu().numpy()), bits(b.cpu().numpy()))
+
+
 def test_decode_and_prefill_orientations_agree(cuda, port):
     import ctypes
 

@@ -1,0 +1,16 @@
+import ctypes, sys, os
+sys.path.insert(0, os.getcwd())
+import torch, numpy as np
+import oracle, paper_2310_04836_b200 as dgq
+M, h, o, g, mode = (int(v) for v in sys.argv[1:6])
+lib = dgq.lib(); lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]; lib.dgq_debug_set_decode(mode)
+port = oracle.port()
+L = oracle.random_layer(h, o, g, seed=7)
+X = port.gen_synthetic(M, h, 3, 3, 50.0, 3)
+out, *_ = port.dgq_forward(X, L)
+D = dgq.DgqLayer(h=L.h, o=L.o, g=L.g, codes=L.codes, s2=L.s2, zp=L.zp, s1=L.s1, k=L.k, act_scale=L.act_scale, mode=L.mode)
+CL = dgq.CudaLayer(D)
+y = CL.forward(torch.from_numpy(X).cuda(), out_dtype=torch.float32)
+torch.cuda.synchronize()
+ok = np.array_equal(y.cpu().numpy().view(np.uint32), out.view(np.uint32))
+print("case", M, h, o, g, mode, CL.plan(M), "bit-exact" if ok else "MISMATCH")
