@@ -607,7 +607,7 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     ms = make_tmap(&tmX, dXq, M, k_pad, ldq, 128u);
     if (ms != DGQ_OK) return ms;
     p.chunk_stride = p.chunk_bytes;
-    DGQ_CUDA(dgq_launch_prefill2(tmX, tmY, p, pl.pdl != 0, st));
+    DGQ_CUDA(dgq_launch_prefill2(tmX, tmY, p, pl.pair_tn, pl.pdl != 0, st));
     return DGQ_OK;
   }
   DGQ_CUDA(dgq_launch_gemm(pl, fused, tmB, tmA, tmY, p, st));

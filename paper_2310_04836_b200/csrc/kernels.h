@@ -107,7 +107,8 @@ cudaError_t dgq_launch_decode(int bn, const CUtensorMap& tmB, const DgqDecodePar
 
 struct DgqGemmPlan {
   int decode;    // 1: K5d (decode.cu) with token tile bn, `ctas` persistent CTAs
-  int prefill2;  // 1: K5p (prefill.cu), persistent CTA pairs, 256 x 256 tiles
+  int prefill2;  // 1: K5p (prefill.cu), persistent CTA pairs, 256 x `pair_tn` tiles
+  int pair_tn;   // 256 or 128 channels per pair tile
   int ctas;
   int bn;
   int nt;  // 128-row weight tiles per CTA
@@ -123,9 +124,9 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
 
 // K5p (prefill.cu): persistent CTA-pair kernel; tmA = Xq with 128-row boxes.
 size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride);
-int dgq_prefill2_clusters(int M, int N);
-cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
-                                cudaStream_t st);
+int dgq_prefill2_clusters(int M, int N, int tn);
+cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,
+                                bool pdl, cudaStream_t st);
 
 cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorMap& tmB, const CUtensorMap& tmA,
                             const CUtensorMap& tmY, const DgqGemmParams& p, cudaStream_t st);

@@ -155,7 +155,7 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 
 // 32 token rows (this warp's TMEM lane quadrant) x 256 channels of one
 // accumulator -> scales -> FP16/FP32 -> swizzled staging -> TMA store.
-template <bool kF16, bool kF16Mode, bool kBias>
+template <int TN, bool kF16, bool kF16Mode, bool kBias>
 __device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase, float rsm, const float* s_s1,
                                          const float* s_bias, uint8_t* stg0, const CUtensorMap* tmY, int nbase,
                                          int mbox) {
@@ -164,7 +164,7 @@ __device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase,
   uint8_t* row0 = stg0 + lane * 128;
   const uint32_t sw = lane & 7;
 #pragma unroll 1
-  for (int c0 = 0; c0 < 256; c0 += kCB) {
+  for (int c0 = 0; c0 < TN; c0 += kCB) {
     if (nbase + c0 >= p.N) break;
     uint32_t r[kCB];
 #pragma unroll
@@ -212,16 +212,22 @@ __device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase,
 
 }  // namespace pf
 
+// TN = pair-tile width in channels: 256 (each CTA dequantises 128 channel
+// rows, one prepared tile) or 128 (each CTA dequantises 64 rows of the SAME
+// prepared tile; twice the tiles, for shapes whose 256-wide tiles leave a
+// ragged last wave).
+template <int TN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     k_dgq_prefill2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
                    const DgqGemmParams p) {
   using namespace pf;
-  constexpr uint32_t kIdesc = idesc_i8(256, 256);
+  constexpr uint32_t kIdesc = idesc_i8(256, TN);
+  constexpr int kRows = TN / 2;  // channel rows of B held (and dequantised) by each CTA
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int KB = p.k_blocks;
   const int n_tiles = (p.N + 127) / 128;  // 128-channel weight tiles (prepared chunks)
-  const int m_pairs = (p.M + 255) / 256, n_pairs = (p.N + 255) / 256;
+  const int m_pairs = (p.M + 255) / 256, n_pairs = (p.N + TN - 1) / TN;
   const int total = m_pairs * n_pairs;
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
@@ -240,8 +246,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
   uint64_t* tempty = tfull + 2;              // [2] leader: both CTAs' epilogues drained it (8 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* s_rs = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
-  float* s_s1 = s_rs + 128;                                // [256]
-  float* s_bias = s_s1 + 256;                              // [256]
+  float* s_s1 = s_rs + 128;                                // [TN]
+  float* s_bias = s_s1 + 256;                              // [TN]
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
@@ -275,7 +281,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       for (int t = cid; t < total; t += ncl) {
         const int mt = t % m_pairs, nt = t / m_pairs;
         const int mrow = mt * 256 + static_cast<int>(rank) * 128;
-        const int ctile = nt * 2 + static_cast<int>(rank);  // this CTA's 128-channel weight tile
+        // the prepared 128-channel weight tile this CTA dequantises (from)
+        const int ctile = TN == 256 ? nt * 2 + static_cast<int>(rank) : nt;
         const bool has_w = ctile < n_tiles;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % kSL;
@@ -299,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         const int acc = tl & 1;
         wait_cluster(&tempty[acc], ((tl >> 1) & 1) ^ 1, 2);  // both epilogues drained this accumulator
         tc_fence_after();
-        const uint32_t d = tm + acc * 256;
+        const uint32_t d = tm + acc * 256;  // accumulator slot (TN <= 256 columns)
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % kSL, b = it % kSB;
           wait_cluster(&ready[b], (it / kSB) & 1, 3);
@@ -327,13 +334,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     // (~1700 cycles for 128 rows on four SMSPs, tools/pf_trace.py), well above
     // the 512-cycle MMA step it feeds.
     const int grp = (warp - 4) >> 2;
-    const int d = static_cast<int>((warp & 3) * 32 + lane);  // channel row of this CTA's B tile
+    (void)kRows;
+    // TN = 256: thread = one of 128 rows, all four 32-k slices; TN = 128: 64 rows x two halves of k
+    const int d = TN == 256 ? static_cast<int>((warp & 3) * 32 + lane) : static_cast<int>((warp & 1) * 32 + lane);
+    const int jbeg = TN == 256 ? 0 : static_cast<int>(((warp & 3) >> 1) * 2);
+    constexpr int kJ = TN == 256 ? 4 : 2;   // 32-k slices per thread
+    const int crow = TN == 256 ? d : static_cast<int>(rank) * 64 + d;  // row inside the prepared chunk
     const uint32_t sw = d & 7;
     const uint32_t ready_leader = mapa(ready, 0);
     int it = 0;
     for (int t = cid; t < total; t += ncl) {
       const int nt = t / m_pairs;
-      const bool has_w = nt * 2 + static_cast<int>(rank) < n_tiles;
+      const bool has_w = (TN == 256 ? nt * 2 + static_cast<int>(rank) : nt) < n_tiles;
       for (int kb = 0; kb < KB; ++kb, ++it) {
         if (it % kDqGroups != grp) continue;
         const int s = it % kSL, b = it % kSB;
@@ -343,22 +355,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         if (has_w) {
           const uint8_t* chunk = sC + s * p.chunk_stride;
           const uint16_t* sc = reinterpret_cast<const uint16_t*>(chunk + 8192);
-          uint4 w4[4];
+          uint4 w4[kJ];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) w4[j] = *reinterpret_cast<const uint4*>(chunk + j * 2048 + d * 16);
+          for (int jj = 0; jj < kJ; ++jj)
+            w4[jj] = *reinterpret_cast<const uint4*>(chunk + (jbeg + jj) * 2048 + crow * 16);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t wv[4] = {w4[j].x, w4[j].y, w4[j].z, w4[j].w};
+          for (int jj = 0; jj < kJ; ++jj) {
+            const int j = jbeg + jj;
+            const uint32_t wv[4] = {w4[jj].x, w4[jj].y, w4[jj].z, w4[jj].w};
             uint32_t o[8];
             if (p.gshift >= 5) {
-              const uint32_t sv = sc[((j * 32) >> p.gshift) * 128 + d];
+              const uint32_t sv = sc[((j * 32) >> p.gshift) * 128 + crow];
               const uint32_t s2 = sv & 0xFFu, bs = dq_bias2(s2, sv >> 8);
 #pragma unroll
               for (int q = 0; q < 4; ++q) dq_word(wv[q], s2, bs, o[2 * q], o[2 * q + 1]);
             } else {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const uint32_t sv = sc[((j * 32 + q * 8) >> p.gshift) * 128 + d];
+                const uint32_t sv = sc[((j * 32 + q * 8) >> p.gshift) * 128 + crow];
                 const uint32_t s2 = sv & 0xFFu;
                 dq_word(wv[q], s2, dq_bias2(s2, sv >> 8), o[2 * q], o[2 * q + 1]);
               }
@@ -369,11 +383,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         } else {
           const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(brow + ((c ^ sw) << 4)) = z;
+          for (int c = 0; c < 2 * kJ; ++c) *reinterpret_cast<uint4*>(brow + (((2 * jbeg + c) ^ sw) << 4)) = z;
         }
         fence_proxy_async_smem();
         named_bar(3 + grp, 128);  // the group's four warps wrote their rows (barrier ids 3..)
-        if (d == 0) arrive_remote_relaxed(ready_leader + b * 8);  // the leader's ready[b]
+        if ((warp & 3) == 0 && lane == 0) arrive_remote_relaxed(ready_leader + b * 8);  // one per group: leader's ready[b]
       }
     }
   } else if (warp >= static_cast<uint32_t>(kEpiWarp0)) {
@@ -388,10 +402,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       const int mt = t % m_pairs, nt = t / m_pairs;
       const int acc = tl & 1;
       const int m0 = mt * 256 + static_cast<int>(rank) * 128;
-      const int n0 = nt * 256;
+      const int n0 = nt * TN;
       // per-tile scales (all four epilogue warps)
       s_rs[e] = (p.rs && m0 + e < p.M) ? p.rs[m0 + e] : 0.0f;
-      for (int i = e; i < 256; i += 128) {
+      for (int i = e; i < TN; i += 128) {
         s_s1[i] = (p.s1 && n0 + i < p.N) ? p.s1[n0 + i] : 0.0f;
         s_bias[i] = (p.bias && n0 + i < p.N) ? p.bias[n0 + i] : 0.0f;
       }
@@ -403,7 +417,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       const float rsm = s_rs[mrow];
       if (p.tma_out && !p.acc_out) {
         const int mbox = m0 + q * 32;
-#define DGQ_EPI2(F16_, MODE_, BIAS_) epi_rows<F16_, MODE_, BIAS_>(p, tbase, rsm, s_s1, s_bias, stg0, &tmY, n0, mbox)
+#define DGQ_EPI2(F16_, MODE_, BIAS_) \
+  epi_rows<TN, F16_, MODE_, BIAS_>(p, tbase, rsm, s_s1, s_bias, stg0, &tmY, n0, mbox)
         const bool b = p.bias != nullptr, f = p.fp16_mode != 0;
         if (p.out_f16) {
           if (f) { if (b) DGQ_EPI2(true, true, true); else DGQ_EPI2(true, true, false); }
@@ -416,7 +431,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       } else {
         const int m = m0 + mrow;
 #pragma unroll 1
-        for (int c0 = 0; c0 < 256; c0 += 16) {
+        for (int c0 = 0; c0 < TN; c0 += 16) {
           if (n0 + c0 >= p.N) break;
           uint32_t r[16];
           tmem_ld16(tbase + c0, r);
@@ -464,22 +479,23 @@ size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride) {
          (2 * pf::kSL + 2 * pf::kSB + 4) * 8 + 16 + (128 + 256 + 256) * 4;
 }
 
-int dgq_prefill2_clusters(int M, int N) {
+int dgq_prefill2_clusters(int M, int N, int tn) {
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int tiles = ((M + 255) / 256) * ((N + tn - 1) / tn);
   const int pairs = sms / 2;
   return tiles < pairs ? tiles : pairs;
 }
 
-cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
-                                cudaStream_t st) {
+template <int TN>
+static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
+                             cudaStream_t st) {
   const size_t smem = dgq_prefill2_smem_bytes(p.chunk_stride);
-  cudaError_t e = cudaFuncSetAttribute(k_dgq_prefill2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  auto kern = k_dgq_prefill2<TN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N));
+  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN));
   cfg.blockDim = dim3(pf::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -488,7 +504,12 @@ cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, 
   attrs[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k_dgq_prefill2, tmA, tmY, p);
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmY, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,
+                                bool pdl, cudaStream_t st) {
+  return tn == 128 ? launch_pf<128>(tmA, tmY, p, pdl, st) : launch_pf<256>(tmA, tmY, p, pdl, st);
 }

@@ -290,14 +290,15 @@ PREFILL_CASES = [
 ]
 
 
-@pytest.fixture
-def pair_kernel():
+@pytest.fixture(params=[256, 128], ids=["tile256", "tile128"])
+def pair_kernel(request):
     import ctypes
 
     lib = dgq.lib()
     lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
-    lib.dgq_debug_set_decode(1 | 0x400)  # route M >= 256 to the CTA-pair kernel (K5p)
-    yield
+    # M >= 256 runs the CTA-pair kernel (K5p); force each pair-tile width
+    lib.dgq_debug_set_decode(1 | 0x400 | (0x800 if request.param == 128 else 0))
+    yield request.param
     lib.dgq_debug_set_decode(1)
 
 
