@@ -594,7 +594,6 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     if (dAcc) ok = ok && (reinterpret_cast<uintptr_t>(dAcc) % 16 == 0) && ((ld_acc * 4) % 16 == 0);
     p.vec_ok = ok ? 1 : 0;
   }
-  (void)ws;
   CUtensorMap tmY{};
   if (pl.bn >= 128 && dY && p.vec_ok) {
     dgq_status ys = make_out_tmap(&tmY, dY, M, N, ldy, out_dtype == DGQ_OUT_F16);
@@ -607,6 +606,12 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     ms = make_tmap(&tmX, dXq, M, k_pad, ldq, 128u);
     if (ms != DGQ_OK) return ms;
     p.chunk_stride = p.chunk_bytes;
+    if (pl.stream_k) {
+      if (!ws) return fail(DGQ_EINVAL, "stream-K prefill kernel needs a workspace");
+      p.stream_k = 1;
+      p.ws = static_cast<int32_t*>(ws);
+      p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
+    }
     DGQ_CUDA(dgq_launch_prefill2(tmX, tmY, p, pl.pair_tn, pl.pdl != 0, st));
     return DGQ_OK;
   }

@@ -569,14 +569,16 @@ extern "C" int dgq_debug_decode_mode() { return g_decode_mode; }
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn, int force_splits) {
   DgqGemmPlan pl{};
   const int kblocks = K_pad / 128;
-  // K5p (CTA pairs, prefill.cu) for M >= 256 when its 256 x 256 pair tiles
-  // fill >= 6 waves of the SM pairs (e.g. OPT-30B fc1 at 2048 tokens: 2569 vs
-  // 2443 TOPS); with fewer tiles the last wave's imbalance costs more than the
-  // pair saves and the one-CTA kernel below runs.
+  // K5p (CTA pairs, prefill.cu) for M >= 256: persistent pairs with a
+  // stream-K split of the (256 x 256 tile, k-block) units, so every pair does
+  // the same MMA work whatever the tile count (the one-CTA kernel below
+  // leaves 1.51 waves of 224 tiles on OPT-30B q/k/v/out/fc2 at 2048 tokens).
   // Tools / tests: mode bit 10 forces K5p, bit 11 forces the 128-wide tile,
-  // bit 12 disables K5p.
+  // bit 12 disables K5p, bit 13 disables stream-K (round-robin whole tiles,
+  // and then K5p only when its tiles fill >= 6 waves of pairs).
+  const bool sk = (g_decode_mode & 0x2000) == 0;
   const long long t256_ = static_cast<long long>((M + 255) / 256) * ((N + 255) / 256);
-  const bool pair_ok = (g_decode_mode & 0x400) != 0 || t256_ >= 6LL * (sm_count() / 2);
+  const bool pair_ok = (g_decode_mode & 0x400) != 0 || sk || t256_ >= 6LL * (sm_count() / 2);
   if (fused && M >= 256 && pair_ok && (g_decode_mode & 0x1000) == 0 && !force_bn && !force_splits &&
       dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128))) <= 232448) {
     const int pairs = sm_count() / 2;
@@ -585,18 +587,22 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
     const double c256 = static_cast<double>((t256 + pairs - 1) / pairs);        // waves x tile time
     const double c128 = 0.5 * static_cast<double>((t128 + pairs - 1) / pairs);
     pl.prefill2 = 1;
-    // the 128-wide tile measured ~40 % slower per tile area (per-k-block fixed
-    // costs against a 256-cycle MMA step; both CTAs stream the whole chunk), so
-    // it is only taken when it saves more than half of the 256-wide tail
-    pl.pair_tn = ((g_decode_mode & 0x800) != 0 || c128 * 1.6 < c256) ? 128 : 256;
+    pl.stream_k = sk ? 1 : 0;
+    // round robin: the 128-wide tile measured ~40 % slower per tile area, so it
+    // is only taken when it saves more than half of the 256-wide tail
+    pl.pair_tn = ((g_decode_mode & 0x800) != 0 || (!sk && c128 * 1.6 < c256)) ? 128 : 256;
     pl.bn = 256;
     pl.nt = pl.pair_tn / 128;
     pl.m_tiles = static_cast<int>(mp);
     pl.n_tiles = (N + 127) / 128;
     pl.splits = 1;
     pl.kb_per_split = kblocks;
-    pl.ctas = 2 * dgq_prefill2_clusters(M, N, pl.pair_tn);
+    pl.ctas = 2 * dgq_prefill2_clusters(M, N, pl.pair_tn, kblocks, sk);
     pl.smem_bytes = dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128)));
+    if (sk) {
+      pl.ws_bytes = static_cast<size_t>(pairs) * kPrefill2SlotBytes;
+      pl.counter_bytes = static_cast<size_t>(pairs) * 2 * 4;
+    }
     pl.pdl = 1;
     return pl;
   }

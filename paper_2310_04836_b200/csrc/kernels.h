@@ -57,6 +57,7 @@ struct DgqGemmParams {
   size_t ldw;
   uint32_t* counters;
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
+  int stream_k;             // K5p: stream-K over (tile, k-block) units (ws / counters = pair slots / flags)
 };
 
 // K5d (decode.cu): stream-K over (weight tile, k-block) units, (code - ZP) as
@@ -109,6 +110,7 @@ struct DgqGemmPlan {
   int decode;    // 1: K5d (decode.cu) with token tile bn, `ctas` persistent CTAs
   int prefill2;  // 1: K5p (prefill.cu), persistent CTA pairs, 256 x `pair_tn` tiles
   int pair_tn;   // 256 or 128 channels per pair tile
+  int stream_k;  // K5p: stream-K work split (workspace = ws_bytes + counter_bytes)
   int ctas;
   int bn;
   int nt;  // 128-row weight tiles per CTA
@@ -124,7 +126,9 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
 
 // K5p (prefill.cu): persistent CTA-pair kernel; tmA = Xq with 128-row boxes.
 size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride);
-int dgq_prefill2_clusters(int M, int N, int tn);
+int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k);
+// stream-K workspace: per pair two CTA partials of 128 x 256 int32, + flags
+constexpr size_t kPrefill2SlotBytes = 2 * 128 * 256 * 4;
 cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,
                                 bool pdl, cudaStream_t st);
 

@@ -153,6 +153,72 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Work decomposition.  Round robin: pair c runs whole tiles c, c + ncl, ...
+// Stream-K (p.stream_k): the tiles x k-blocks units are cut into ncl equal
+// contiguous ranges, one per pair, so every pair does the same MMA work
+// whatever the tile count (e.g. 224 tiles of OPT-30B q_proj at 2048 tokens
+// over 74 pairs = 3.03 tiles each instead of 4 waves).  A range is a sequence
+// of segments (tile t, k-blocks [lo, hi)); only the FIRST segment of a range
+// can start inside a tile (lo > 0, a "contributor": its int32 partial goes to
+// the pair's workspace slot) and only the LAST can end inside one (lo == 0,
+// hi < KB, the "owner": it adds the contributors' partials — exact integer
+// sums — before the epilogue).  Owners run at the end of their range and
+// contributors at the start of theirs, so the owner's wait is normally over
+// before it begins; all pairs are co-resident (grid <= active clusters).
+struct SegIter {
+  long long u, uend;  // stream-K: current / end unit
+  int t, total, step, KB, sk;
+  __device__ SegIter(const DgqGemmParams& p, int cid, int ncl, int total_, int KB_)
+      : t(cid), total(total_), step(ncl), KB(KB_), sk(p.stream_k) {
+    const long long U = static_cast<long long>(total_) * KB_;
+    u = U * cid / ncl;
+    uend = U * (cid + 1) / ncl;
+  }
+  __device__ bool next(int& tile, int& lo, int& hi) {
+    if (sk) {
+      if (u >= uend) return false;
+      tile = static_cast<int>(u / KB);
+      lo = static_cast<int>(u - static_cast<long long>(tile) * KB);
+      const long long tend = static_cast<long long>(tile + 1) * KB;
+      hi = static_cast<int>((uend < tend ? uend : tend) - static_cast<long long>(tile) * KB);
+      u = static_cast<long long>(tile) * KB + hi;
+      return true;
+    }
+    if (t >= total) return false;
+    tile = t;
+    lo = 0;
+    hi = KB;
+    t += step;
+    return true;
+  }
+};
+__device__ __forceinline__ long long sk_begin(long long U, int c, int ncl) { return U * c / ncl; }
+
+__device__ __forceinline__ void st_release_gpu(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+// r[0..15] += the contributors' partials of 16 columns (chunk c16 of this
+// thread's row).  part: first contributor's slot + row offset; pstride: ints
+// between consecutive pairs' slots.  Layout per slot: [c16][row][16] int32.
+__device__ __forceinline__ void add_partials16(uint32_t* r, const int32_t* part, int npart, size_t pstride, int c16) {
+  for (int pi = 0; pi < npart; ++pi) {
+    const int4* s = reinterpret_cast<const int4*>(part + pi * pstride + static_cast<size_t>(c16) * 2048);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int4 x = __ldcg(s + v);
+      r[4 * v + 0] += static_cast<uint32_t>(x.x);
+      r[4 * v + 1] += static_cast<uint32_t>(x.y);
+      r[4 * v + 2] += static_cast<uint32_t>(x.z);
+      r[4 * v + 3] += static_cast<uint32_t>(x.w);
+    }
+  }
+}
+
 // 32 token rows (this warp's TMEM lane quadrant) x 256 channels of one
 // accumulator -> scales -> FP16/FP32 -> swizzled staging -> TMA store.
 template <int TN, bool kF16, bool kF16Mode, bool kBias>
@@ -278,13 +344,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     if (lane == 0) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // Xq / row scales come from K1
       int it = 0;
-      for (int t = cid; t < total; t += ncl) {
+      SegIter si(p, cid, ncl, total, KB);
+      int t, lo, hi;
+      while (si.next(t, lo, hi)) {
         const int mt = t % m_pairs, nt = t / m_pairs;
         const int mrow = mt * 256 + static_cast<int>(rank) * 128;
         // the prepared 128-channel weight tile this CTA dequantises (from)
         const int ctile = TN == 256 ? nt * 2 + static_cast<int>(rank) : nt;
         const bool has_w = ctile < n_tiles;
-        for (int kb = 0; kb < KB; ++kb, ++it) {
+        for (int kb = lo; kb < hi; ++kb, ++it) {
           const int s = it % kSL;
           wait_local(&empty[s], ((it / kSL) & 1) ^ 1, 1);
           // a token half entirely past M is not loaded: its rows of D are never stored
@@ -302,12 +370,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     if (leader) {
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       int it = 0, tl = 0;
-      for (int t = cid; t < total; t += ncl, ++tl) {
+      SegIter si(p, cid, ncl, total, KB);
+      int t, lo, hi;
+      for (; si.next(t, lo, hi); ++tl) {
         const int acc = tl & 1;
         wait_cluster(&tempty[acc], ((tl >> 1) & 1) ^ 1, 2);  // both epilogues drained this accumulator
         tc_fence_after();
         const uint32_t d = tm + acc * 256;  // accumulator slot (TN <= 256 columns)
-        for (int kb = 0; kb < KB; ++kb, ++it) {
+        for (int kb = lo; kb < hi; ++kb, ++it) {
           const int s = it % kSL, b = it % kSB;
           wait_cluster(&ready[b], (it / kSB) & 1, 3);
           if (p.dbg && blockIdx.x == 0 && lane == 0 && it < 1024) {  // tools/pf_trace.py
@@ -319,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
           const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kATile));
           const uint64_t db = umma_desc_sw128(smem_u32(sB + b * kBTile));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) mma2_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb | kk) != 0);
+          for (int kk = 0; kk < 4; ++kk) mma2_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb != lo) || kk != 0);
           commit2_mc(&empty[s]);
           commit2_mc(&bempty[b]);
         }
@@ -343,10 +413,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     const uint32_t sw = d & 7;
     const uint32_t ready_leader = mapa(ready, 0);
     int it = 0;
-    for (int t = cid; t < total; t += ncl) {
+    SegIter si(p, cid, ncl, total, KB);
+    int t, lo, hi;
+    while (si.next(t, lo, hi)) {
       const int nt = t / m_pairs;
       const bool has_w = (TN == 256 ? nt * 2 + static_cast<int>(rank) : nt) < n_tiles;
-      for (int kb = 0; kb < KB; ++kb, ++it) {
+      for (int kb = lo; kb < hi; ++kb, ++it) {
         if (it % kDqGroups != grp) continue;
         const int s = it % kSL, b = it % kSB;
         wait_local(&full[s], (it / kSL) & 1, 4);
@@ -398,22 +470,79 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     uint8_t* stg0 = sStg + (warp - kEpiWarp0) * 4096;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // row scales from K1
     int tl = 0;
-    for (int t = cid; t < total; t += ncl, ++tl) {
+    SegIter si(p, cid, ncl, total, KB);
+    const long long U = static_cast<long long>(total) * KB;
+    constexpr size_t kSlot = 128 * TN;  // ints per CTA partial
+    const size_t pstride = 2 * kSlot;   // ints between pairs' slots
+    int t, lo, hi;
+    for (; si.next(t, lo, hi); ++tl) {
       const int mt = t % m_pairs, nt = t / m_pairs;
       const int acc = tl & 1;
       const int m0 = mt * 256 + static_cast<int>(rank) * 128;
       const int n0 = nt * TN;
+      const uint32_t tbase = tmem + ((q * 32) << 16) + acc * 256;
+      const int mrow = q * 32 + lane;
+      if (lo > 0) {
+        // stream-K contributor: park the int32 partial in this pair's slot
+        wait_local(&tfull[acc], (tl >> 1) & 1, 5);
+        tc_fence_after();
+        int32_t* slot = p.ws + (static_cast<size_t>(cid) * 2 + rank) * kSlot + static_cast<size_t>(mrow) * 16;
+#pragma unroll 1
+        for (int c0 = 0; c0 < TN; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tbase + c0, r);
+          tmem_ld_wait();
+          int4* dst = reinterpret_cast<int4*>(slot + static_cast<size_t>(c0 / 16) * 2048);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            __stcg(dst + v, make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
+                                      static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3])));
+        }
+        __threadfence();
+        tc_fence_before();
+        named_bar(2, 128);
+        if (e == 0) st_release_gpu(p.counters + cid * 2 + rank, 1u);
+        __syncwarp();
+        if (lane == 0) arrive_remote(tempty_leader + acc * 8);
+        continue;
+      }
+      // owner of a split tile: the pairs after this one whose ranges start inside it
+      int npart = 0;
+      if (hi < KB) {
+        const long long tend = static_cast<long long>(t + 1) * KB;
+        while (cid + 1 + npart < ncl && sk_begin(U, cid + 1 + npart, ncl) < tend) ++npart;
+      }
       // per-tile scales (all four epilogue warps)
       s_rs[e] = (p.rs && m0 + e < p.M) ? p.rs[m0 + e] : 0.0f;
       for (int i = e; i < TN; i += 128) {
         s_s1[i] = (p.s1 && n0 + i < p.N) ? p.s1[n0 + i] : 0.0f;
         s_bias[i] = (p.bias && n0 + i < p.N) ? p.bias[n0 + i] : 0.0f;
       }
+      if (npart) {
+        for (int c = 1; c <= npart; ++c) {
+          long long n = 0;
+          while (ld_acquire_gpu(p.counters + (cid + c) * 2 + rank) == 0) watchdog(n, 9, 0);
+        }
+      }
       named_bar(2, 128);
+      if (npart && e == 0)  // every thread has seen the flags: re-arm them for the next launch
+        for (int c = 1; c <= npart; ++c) p.counters[(cid + c) * 2 + rank] = 0u;
+      const int32_t* part =
+          npart ? p.ws + (static_cast<size_t>(cid + 1) * 2 + rank) * kSlot + static_cast<size_t>(mrow) * 16 : nullptr;
       wait_local(&tfull[acc], (tl >> 1) & 1, 5);
       tc_fence_after();
-      const uint32_t tbase = tmem + ((q * 32) << 16) + acc * 256;
-      const int mrow = q * 32 + lane;
+      if (npart) {
+        // fold the contributors' partials into this thread's TMEM row (exact int32)
+#pragma unroll 1
+        for (int c0 = 0; c0 < TN; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tbase + c0, r);
+          tmem_ld_wait();
+          add_partials16(r, part, npart, pstride, c0 / 16);
+          tmem_st16(tbase + c0, r);
+        }
+        tmem_st_wait();
+      }
       const float rsm = s_rs[mrow];
       if (p.tma_out && !p.acc_out) {
         const int mbox = m0 + q * 32;
@@ -479,12 +608,37 @@ size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride) {
          (2 * pf::kSL + 2 * pf::kSB + 4) * 8 + 16 + (128 + 256 + 256) * 4;
 }
 
-int dgq_prefill2_clusters(int M, int N, int tn) {
+template <int TN>
+static int max_active_pairs() {
+  // persistent + stream-K spin-waits need every pair co-resident: ask the
+  // occupancy calculator how many 2-CTA clusters of this kernel fit at once
+  static int cached[2] = {0, 0};
+  int& c = cached[TN == 256 ? 0 : 1];
+  if (c) return c;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = ((M + 255) / 256) * ((N + tn - 1) / tn);
-  const int pairs = sms / 2;
-  return tiles < pairs ? tiles : pairs;
+  int n = sms / 2;
+  const size_t smem = dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(128)));
+  auto kern = k_dgq_prefill2<TN>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
+      cudaSuccess) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * n);
+    cfg.blockDim = dim3(pf::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    int q = 0;
+    if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0 && q < n) n = q;
+  }
+  cudaGetLastError();
+  c = n;
+  return c;
+}
+
+int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k) {
+  const int pairs = tn == 128 ? max_active_pairs<128>() : max_active_pairs<256>();
+  const long long tiles = static_cast<long long>((M + 255) / 256) * ((N + tn - 1) / tn);
+  const long long work = stream_k ? tiles * k_blocks : tiles;
+  return static_cast<int>(work < pairs ? work : pairs);
 }
 
 template <int TN>
@@ -495,7 +649,7 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN));
+  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN, p.k_blocks, p.stream_k != 0));
   cfg.blockDim = dim3(pf::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

@@ -287,17 +287,25 @@ def test_decode_kernel_matches_oracle(cuda, port, M, h, o, g):
 PREFILL_CASES = [
     # (M, h, o, g): persistent CTA-pair kernel (M >= 256): ragged M / N / K, odd tile counts, every group path
     (256, 512, 256, 128), (300, 1024, 384, 64), (513, 992, 1000, 32), (777, 2048, 640, 256), (1030, 384, 130, 128),
+
+
+    # stream-K over many pairs: tiles split across 3+ pairs, owners with several contributors
+    (1024, 2048, 1792, 128), (512, 7168, 768, 128),
 ]
 
+# debug mode bits (csrc/gemm.cu dgq_plan_gemm): 0x400 force K5p, 0x800 128-wide
+# pair tile, 0x2000 round-robin whole tiles instead of stream-K
+PAIR_MODES = {"sk256": 0x400, "sk128": 0x400 | 0x800, "rr256": 0x400 | 0x2000, "rr128": 0x400 | 0x800 | 0x2000}
 
-@pytest.fixture(params=[256, 128], ids=["tile256", "tile128"])
+
+@pytest.fixture(params=list(PAIR_MODES), ids=list(PAIR_MODES))
 def pair_kernel(request):
     import ctypes
 
     lib = dgq.lib()
     lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
-    # M >= 256 runs the CTA-pair kernel (K5p); force each pair-tile width
-    lib.dgq_debug_set_decode(1 | 0x400 | (0x800 if request.param == 128 else 0))
+    # M >= 256 runs the CTA-pair kernel (K5p); force each work split / tile width
+    lib.dgq_debug_set_decode(1 | PAIR_MODES[request.param])
     yield request.param
     lib.dgq_debug_set_decode(1)
 
@@ -321,6 +329,36 @@ def test_prefill_pair_kernel_matches_oracle(cuda, port, pair_kernel, M, h, o, g)
         assert np.array_equal(bits(y32b.cpu().numpy()), bits(out))
         y16 = CL.linear(codes, drs, bias=db, out_dtype=torch.float16)
         assert np.array_equal(bits(y16.cpu().numpy()), bits(port.fp16_round_array(out).astype(np.float16)))
+
+
+@pytest.mark.parametrize("M,h,o", [(2048, 7168, 7168), (512, 7168, 28672)])
+def test_prefill_full_size_work_splits_agree(cuda, port, M, h, o):
+    # OPT-30B shapes: stream-K pairs, round-robin pairs and the one-CTA kernel
+    # produce identical int32 accumulators; sampled rows equal the oracle
+    import ctypes
+
+    lib = dgq.lib()
+    lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    L = oracle.random_layer(h, o, 128, seed=o)
+    X = port.gen_synthetic(M, h, 5, 3, 50.0, 3)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+    accs = {}
+    try:
+        for name, mode in (("sk", 1), ("rr", 1 | 0x2000), ("one_cta", 1 | 0x1000)):
+            lib.dgq_debug_set_decode(mode)
+            y, acc = CL.linear(codes, drs, out_dtype=torch.float16, want_acc=True)
+            y2 = CL.linear(codes, drs, out_dtype=torch.float16)  # TMA-store epilogue path
+            assert torch.equal(y.view(torch.int16), y2.view(torch.int16)), name
+            accs[name] = acc
+    finally:
+        lib.dgq_debug_set_decode(1)
+    assert torch.equal(accs["sk"], accs["rr"])
+    assert torch.equal(accs["sk"], accs["one_cta"])
+    w = CL.dequant_s8().cpu().numpy().astype(np.int64)
+    q = codes[:, :h].cpu().numpy().astype(np.int64)
+    rows = np.random.default_rng(0).choice(M, 6, replace=False)
+    assert np.array_equal(accs["sk"][rows].cpu().numpy(), (q[rows] @ w).astype(np.int32))
 
 
 @pytest.mark.parametrize("M", [1, 13, 32, 40])
