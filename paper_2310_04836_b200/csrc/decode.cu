@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
       for (w.next(KB, ku); w.valid(); w.next(KB, ku)) issue(w, true, true);
       asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
+    __syncwarp();  // lanes 1-31 wait here, not at the CTA barrier (see prefill.cu)
   } else if (warp <= kMmaWarps) {
     // ------------------------------ MMA issuers ----------------------------
     // A single thread issues a tcgen05.mma only every ~50 cycles (issue

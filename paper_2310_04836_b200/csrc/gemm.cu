@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(Cfg<BN, NT, SL, SA, DQW, kFused>::kThreads, 1)
         tma_load_2d(sB + s * kBBytes, &tmB, &full_l[s], (kb0 + i) * 128, mt * BN);
       }
     }
+    __syncwarp();  // lanes 1-31 wait here, not at the CTA barrier (see prefill.cu)
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ----------------------------
     if (lane == 0) {

@@ -42,11 +42,18 @@
 namespace dgqk {
 namespace pf {
 
-constexpr int kSL = 5;            // Xq tile + packed-chunk stages (k-blocks in flight)
+// Three rings, sized from the measured chain (tools/pf_trace.py): a bulk copy
+// lands ~0.5-0.8 us after issue and a group dequantises a k-block in ~0.8 us,
+// against a 0.26 us MMA step, so the packed chunks are fetched kLag k-blocks
+// ahead of the Xq tiles and released by the dequantisers (not the MMA).
+constexpr int kSA = 5;            // Xq tile stages (released by the MMA)
+constexpr int kSC = 7;            // packed-chunk stages (released by the dequantisers)
+constexpr int kLag = kSC - kSA;   // chunk i is issued together with Xq tile i - kLag
 constexpr int kSB = 4;            // dequantised weight-tile slots (> dequant groups: a group can run ahead)
 constexpr int kDqGroups = 3;      // groups of four dequant warps, alternate k-blocks
 constexpr int kEpiWarp0 = 4 + 4 * kDqGroups;  // first of the four epilogue warps
-constexpr int kThreads = 32 * (kEpiWarp0 + 4);
+constexpr int kXWarp = kEpiWarp0 + 4;         // second Xq-tile producer warp
+constexpr int kThreads = 32 * (kXWarp + 1);
 constexpr uint32_t kATile = 128 * 128;   // 128 token rows x 128 k (bytes)
 constexpr uint32_t kBTile = 128 * 128;   // 128 channel rows x 128 k
 constexpr uint32_t kStaging = 4 * 4096;  // epilogue: one 4 KB staging buffer per epilogue warp
@@ -111,6 +118,28 @@ __device__ __forceinline__ void watchdog(long long& n, int id, uint32_t parity) 
   if (n > (1ll << 25)) __trap();
 #endif
 }
+// non-blocking probe of a local barrier phase
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// 2-D TMA load into this CTA's smem whose completion is signalled on an
+// mbarrier of either CTA of the pair (here: the leader's), so the leader's
+// MMA issuer learns directly that both halves of the Xq tile have landed.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity, int id = 0) {
   long long n = 0;
   while (!try_wait_cluster(bar, parity)) watchdog(n, id, parity);
@@ -174,6 +203,35 @@ struct SegIter {
     u = U * cid / ncl;
     uend = U * (cid + 1) / ncl;
   }
+  // units of this pair and the (tile, k-block) of its i-th unit
+  __device__ int count() const {
+    if (sk) return static_cast<int>(uend - u);  // valid before the first next()
+    const int mine = t < total ? (total - 1 - t) / step + 1 : 0;
+    return mine * KB;
+  }
+  // A division-free cursor over the pair's units: the producer and the
+  // dequantisers step through units one (or kDqGroups) at a time, and a 64-bit
+  // division per unit costs a lone producer thread ~0.5 us (tools/pf_trace.py).
+  struct Cursor {
+    int t, kb;
+  };
+  __device__ Cursor first() const {
+    Cursor c;
+    if (sk) {
+      c.t = static_cast<int>(u / KB);
+      c.kb = static_cast<int>(u - static_cast<long long>(c.t) * KB);
+    } else {
+      c.t = t;
+      c.kb = 0;
+    }
+    return c;
+  }
+  __device__ void advance(Cursor& c) const {
+    if (++c.kb == KB) {
+      c.kb = 0;
+      c.t += sk ? 1 : step;
+    }
+  }
   __device__ bool next(int& tile, int& lo, int& hi) {
     if (sk) {
       if (u >= uend) return false;
@@ -192,6 +250,14 @@ struct SegIter {
     return true;
   }
 };
+// tools/pf_trace.py: globaltimer stamps of CTA 0, dbg[slot * 1024 + k-block]
+__device__ __forceinline__ void pf_stamp(const DgqGemmParams& p, int slot, int it) {
+  if (p.dbg && blockIdx.x == 0 && it < 1024) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.dbg[slot * 1024 + it] = g;
+  }
+}
 __device__ __forceinline__ long long sk_begin(long long U, int c, int ncl) { return U * c / ncl; }
 
 __device__ __forceinline__ void st_release_gpu(uint32_t* a, uint32_t v) {
@@ -299,14 +365,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
 
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = sm;                          // [kSL][128 x 128] Xq (SW128 K-major)
-  uint8_t* sB = sA + kSL * kATile;           // [kSB][128 x 128] W_s8 (SW128 K-major)
+  uint8_t* sA = sm;                          // [kSA][128 x 128] Xq (SW128 K-major)
+  uint8_t* sB = sA + kSA * kATile;           // [kSB][128 x 128] W_s8 (SW128 K-major)
   uint8_t* sStg = sB + kSB * kBTile;         // epilogue staging
-  uint8_t* sC = sStg + kStaging;             // [kSL][chunk_stride] packed chunks
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kSL * p.chunk_stride);
-  uint64_t* full = bars;                     // [kSL] A tile + chunk landed (local)
-  uint64_t* empty = full + kSL;              // [kSL] MMA done with the stage (multicast commit)
-  uint64_t* ready = empty + kSL;             // [kSB] leader: both CTAs' B slot dequantised (2 arrivals)
+  uint8_t* sC = sStg + kStaging;             // [kSC][chunk_stride] packed chunks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kSC * p.chunk_stride);
+  uint64_t* afull = bars;                    // [kSA] leader: both CTAs' Xq halves landed (pair TMA tx)
+  uint64_t* aempty = afull + kSA;            // [kSA] MMA done with the Xq tile (multicast commit)
+  uint64_t* cfull = aempty + kSA;            // [kSC] packed chunk landed (local)
+  uint64_t* cempty = cfull + kSC;            // [kSC] dequantised (one arrive by the group)
+  uint64_t* ready = cempty + kSC;            // [kSB] leader: both CTAs' B slot dequantised (2 arrivals)
   uint64_t* bempty = ready + kSB;            // [kSB] MMA done with the B slot (multicast commit)
   uint64_t* tfull = bempty + kSB;            // [2] accumulator complete (multicast commit)
   uint64_t* tempty = tfull + 2;              // [2] leader: both CTAs' epilogues drained it (8 arrivals)
@@ -317,9 +385,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSL; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kSA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < kSC; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 1);
     }
     for (int b = 0; b < kSB; ++b) {
       mbar_init(&ready[b], 2);
@@ -339,32 +411,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------ producer ------------------------------
+  if (warp == 0 || warp == 2) {
+    // ------------------------ chunk producers (2 warps) ------------------------
+    // A TMA/bulk-copy instruction holds its issuing warp for ~650-850 cycles
+    // (tools/l2_stream.cu: one lone issuing thread streams one request per
+    // ~660 cycles whatever its size; N issuing warps stream N times that), so
+    // each operand stream has two issuing warps taking alternate k-blocks.
+    // Packed chunks run up to kSC k-blocks ahead (freed by the dequantisers);
+    // they do not depend on the previous kernel, so no griddepcontrol.wait.
     if (lane == 0) {
-      asm volatile("griddepcontrol.wait;" ::: "memory");  // Xq / row scales come from K1
-      int it = 0;
+      const int w = warp == 0 ? 0 : 1;
       SegIter si(p, cid, ncl, total, KB);
-      int t, lo, hi;
-      while (si.next(t, lo, hi)) {
-        const int mt = t % m_pairs, nt = t / m_pairs;
-        const int mrow = mt * 256 + static_cast<int>(rank) * 128;
+      const int n = si.count();
+      SegIter::Cursor c = si.first();
+      if (w) si.advance(c);
+      for (int i = w; i < n; i += 2) {
+        const int t = c.t, kb = c.kb;
+        si.advance(c);
+        si.advance(c);
+        const int nt = t / m_pairs;
         // the prepared 128-channel weight tile this CTA dequantises (from)
         const int ctile = TN == 256 ? nt * 2 + static_cast<int>(rank) : nt;
         const bool has_w = ctile < n_tiles;
-        for (int kb = lo; kb < hi; ++kb, ++it) {
-          const int s = it % kSL;
-          wait_local(&empty[s], ((it / kSL) & 1) ^ 1, 1);
-          // a token half entirely past M is not loaded: its rows of D are never stored
-          const bool has_a = mrow < p.M;
-          mbar_arrive_expect_tx(&full[s], (has_a ? kATile : 0u) + (has_w ? p.chunk_bytes : 0u));
-          if (has_a) tma_load_2d(sA + s * kATile, &tmA, &full[s], kb * 128, mrow);
-          if (has_w)
-            bulk_load(sC + s * p.chunk_stride, p.tiles + (static_cast<size_t>(ctile) * KB + kb) * p.chunk_bytes,
-                      p.chunk_bytes, &full[s]);
-        }
+        const int s = i % kSC;
+        wait_local(&cempty[s], ((i / kSC) & 1) ^ 1, 1);
+        pf_stamp(p, 1, i);
+        mbar_arrive_expect_tx(&cfull[s], has_w ? p.chunk_bytes : 0u);
+        if (has_w)
+          bulk_load(sC + s * p.chunk_stride, p.tiles + (static_cast<size_t>(ctile) * KB + kb) * p.chunk_bytes,
+                    p.chunk_bytes, &cfull[s]);
       }
     }
+    __syncwarp();  // lanes 1-31 park here (a lone lane next to a warp parked at a CTA/cluster barrier issues slowly)
+  } else if (warp == 3 || warp == static_cast<uint32_t>(kXWarp)) {
+    // ------------------------ Xq-tile producers (2 warps) ------------------------
+    // Each CTA loads its 128 token rows; the copy signals the LEADER's afull
+    // (cta_group::2 TMA), which expects both halves' bytes.
+    if (lane == 0) {
+      const int w = warp == 3 ? 0 : 1;
+      const uint32_t afull_leader = mapa(afull, 0);
+      SegIter si(p, cid, ncl, total, KB);
+      const int n = si.count();
+      SegIter::Cursor c = si.first();
+      if (w) si.advance(c);
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // Xq / row scales come from K1
+      for (int i = w; i < n; i += 2) {
+        const int t = c.t, kb = c.kb;
+        si.advance(c);
+        si.advance(c);
+        const int s = i % kSA;
+        wait_local(&aempty[s], ((i / kSA) & 1) ^ 1, 7);
+        const int mpair = (t % m_pairs) * 256;
+        // a token half entirely past M is not loaded: its rows of D are never stored
+        if (leader)
+          mbar_arrive_expect_tx(&afull[s], (mpair < p.M ? kATile : 0u) + (mpair + 128 < p.M ? kATile : 0u));
+        const int mrow = mpair + static_cast<int>(rank) * 128;
+        if (mrow < p.M) tma_load_2d_pair(sA + s * kATile, &tmA, afull_leader + s * 8, kb * 128, mrow);
+        pf_stamp(p, 5, i);
+      }
+    }
+    __syncwarp();
   } else if (warp == 1) {
     // --------------------- MMA issuer (leader CTA, converged warp) ---------------------
     if (leader) {
@@ -378,8 +484,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         tc_fence_after();
         const uint32_t d = tm + acc * 256;  // accumulator slot (TN <= 256 columns)
         for (int kb = lo; kb < hi; ++kb, ++it) {
-          const int s = it % kSL, b = it % kSB;
-          wait_cluster(&ready[b], (it / kSB) & 1, 3);
+          const int s = it % kSA, b = it % kSB;
+          wait_cluster(&ready[b], (it / kSB) & 1, 3);  // both CTAs' B slots dequantised
+          wait_cluster(&afull[s], (it / kSA) & 1, 7);  // both CTAs' Xq halves landed
           if (p.dbg && blockIdx.x == 0 && lane == 0 && it < 1024) {  // tools/pf_trace.py
             uint64_t g;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
@@ -390,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
           const uint64_t db = umma_desc_sw128(smem_u32(sB + b * kBTile));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) mma2_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb != lo) || kk != 0);
-          commit2_mc(&empty[s]);
+          commit2_mc(&aempty[s]);
           commit2_mc(&bempty[b]);
         }
         commit2_mc(&tfull[acc]);
@@ -412,17 +519,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     const int crow = TN == 256 ? d : static_cast<int>(rank) * 64 + d;  // row inside the prepared chunk
     const uint32_t sw = d & 7;
     const uint32_t ready_leader = mapa(ready, 0);
-    int it = 0;
     SegIter si(p, cid, ncl, total, KB);
-    int t, lo, hi;
-    while (si.next(t, lo, hi)) {
-      const int nt = t / m_pairs;
-      const bool has_w = (TN == 256 ? nt * 2 + static_cast<int>(rank) : nt) < n_tiles;
-      for (int kb = lo; kb < hi; ++kb, ++it) {
-        if (it % kDqGroups != grp) continue;
-        const int s = it % kSL, b = it % kSB;
-        wait_local(&full[s], (it / kSL) & 1, 4);
+    const int n = si.count();
+    SegIter::Cursor cu = si.first();
+    for (int i = 0; i < grp; ++i) si.advance(cu);
+    {
+      for (int it = grp; it < n; it += kDqGroups) {
+        const int t = cu.t;
+        for (int i = 0; i < kDqGroups; ++i) si.advance(cu);
+        const int nt = t / m_pairs;
+        const bool has_w = (TN == 256 ? nt * 2 + static_cast<int>(rank) : nt) < n_tiles;
+        const int s = it % kSC, b = it % kSB;
+        wait_local(&cfull[s], (it / kSC) & 1, 4);
+        if ((warp & 3) == 0 && lane == 0) pf_stamp(p, 2, it);
         wait_local(&bempty[b], ((it / kSB) & 1) ^ 1, 6);
+        if ((warp & 3) == 0 && lane == 0) pf_stamp(p, 3, it);
         uint8_t* brow = sB + b * kBTile + (d >> 3) * 1024 + (d & 7) * 128;
         if (has_w) {
           const uint8_t* chunk = sC + s * p.chunk_stride;
@@ -459,10 +570,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         }
         fence_proxy_async_smem();
         named_bar(3 + grp, 128);  // the group's four warps wrote their rows (barrier ids 3..)
-        if ((warp & 3) == 0 && lane == 0) arrive_remote_relaxed(ready_leader + b * 8);  // one per group: leader's ready[b]
+        if ((warp & 3) == 0 && lane == 0) {
+          pf_stamp(p, 4, it);
+          mbar_arrive(&cempty[s]);  // the chunk has been read
+          arrive_remote_relaxed(ready_leader + b * 8);  // one per group: leader's ready[b]
+        }
       }
     }
-  } else if (warp >= static_cast<uint32_t>(kEpiWarp0)) {
+  } else if (warp >= static_cast<uint32_t>(kEpiWarp0) && warp < static_cast<uint32_t>(kXWarp)) {
     // ------------------------------ epilogue ------------------------------
     const int e = threadIdx.x - 32 * kEpiWarp0;      // 0..127 = token row of this CTA's D
     const uint32_t q = warp & 3;                     // TMEM lane quadrant
@@ -604,8 +719,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
 using namespace dgqk;
 
 size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride) {
-  return 1024 + pf::kSL * (pf::kATile + chunk_stride) + pf::kSB * pf::kBTile + pf::kStaging +
-         (2 * pf::kSL + 2 * pf::kSB + 4) * 8 + 16 + (128 + 256 + 256) * 4;
+  return 1024 + pf::kSA * pf::kATile + pf::kSC * chunk_stride + pf::kSB * pf::kBTile + pf::kStaging +
+         (2 * pf::kSA + 2 * pf::kSC + 2 * pf::kSB + 4) * 8 + 16 + (128 + 256 + 256) * 4;
 }
 
 template <int TN>

@@ -1,5 +1,7 @@
-"""K5p per-k-block timeline of the first CTA pair (globaltimer, us): when the
-leader's MMA issuer observes each k-block ready, and the median period.  python tools/pf_trace.py M K N"""
+"""K5p per-k-block timeline of CTA 0 (the first pair's leader), globaltimer us:
+producer issue (empty slot free), dequant group saw data (full), saw its B
+slot free (bempty), finished (group barrier), MMA issuer saw both CTAs ready.
+python tools/pf_trace.py M K N [mode]"""
 import ctypes as C
 import os
 import sys
@@ -11,6 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2310_04836_b200 as dgq  # noqa: E402
 
 M, K, N = (int(v) for v in sys.argv[1:4])
+mode = int(sys.argv[4], 0) if len(sys.argv) > 4 else 0x400
 L = dgq.random_layer(K, N, 128, seed=1)
 CL = dgq.CudaLayer(L, validate=False)
 x = torch.randn(M, K, device="cuda") * 3
@@ -20,7 +23,7 @@ buf = torch.zeros(9 * 1024, dtype=torch.int64, device="cuda")
 lib = dgq.lib()
 lib.dgq_debug_set_timestamps.argtypes = [C.c_void_p]
 lib.dgq_debug_set_decode.argtypes = [C.c_int]
-lib.dgq_debug_set_decode(1 | 0x400)
+lib.dgq_debug_set_decode(1 | mode)
 for _ in range(2):
     CL.linear(codes, rs, out=out)
 torch.cuda.synchronize()
@@ -28,14 +31,18 @@ lib.dgq_debug_set_timestamps(C.c_void_p(buf.data_ptr()))
 CL.linear(codes, rs, out=out)
 torch.cuda.synchronize()
 lib.dgq_debug_set_timestamps(None)
-b = buf.view(9, 1024).cpu().numpy()
-t0 = b[b > 0].min()
-r = lambda v: (v - t0) / 1e3  # noqa: E731
-print(" kb | lead: start  slot-ok  arrive | peer: start  slot-ok  arrive | mma ready")
-for i in list(range(0, 6)) + list(range(60, 69)):
-    print(f"{i:3d} | {r(b[3][i]):6.2f} {r(b[5][i]):6.2f} {r(b[1][i]):6.2f} | {r(b[4][i]):6.2f} {r(b[6][i]):6.2f} "
-          f"{r(b[2][i]):6.2f} | {r(b[0][i]):6.2f}")
+b = buf.view(9, 1024).cpu().numpy().astype(np.float64)
 n = int((b[0] > 0).sum())
+t0 = b[:5, :n][b[:5, :n] > 0].min()
+r = lambda v: (v - t0) / 1e3 if v > 0 else float("nan")  # noqa: E731
+print(" kb | issue   full  bempty  dq-done | mma    | A-issue  loop#")
+for i in list(range(0, 12)) + list(range(100, 124)):
+    if i < n:
+        print(f"{i:3d} | {r(b[1][i]):6.2f} {r(b[2][i]):6.2f} {r(b[3][i]):6.2f} {r(b[4][i]):6.2f} | {r(b[0][i]):6.2f} | "
+              f"{r(b[5][i]):6.2f} {int(b[6][i]) if b[6][i] else 0:8d}")
 d = np.diff(b[0][:n]) / 1e3
 print(f"MMA period median {np.median(d):.3f} us over {n} k-blocks")
+lat = lambda a, c: np.median((b[c][:n] - b[a][:n]) / 1e3)  # noqa: E731
+print(f"median: issue->full {lat(1, 2):.3f}  full->bempty {lat(2, 3):.3f}  bempty->done {lat(3, 4):.3f}  "
+      f"done->mma {lat(4, 0):.3f}  issue->mma {lat(1, 0):.3f} us")
 lib.dgq_debug_set_decode(1)
