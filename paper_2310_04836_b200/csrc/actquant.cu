@@ -225,11 +225,36 @@ __global__ void __launch_bounds__(T) k_actquant_h_any(const __half* __restrict__
 // thread first issues all of its V 16-B (f16) or 32-B (f32) loads, then divides
 // by k with the hoisted reciprocal (div_k), reduces the row absmax (block, then
 // over the cluster through DSMEM), and quantises from registers.
+// x' = x / k for one 8-channel chunk c.  kone[c] != 0 marks a chunk whose eight
+// k are exactly 1 (compute_smooth, proj/src/smoothing.cpp:45-47, gives k =
+// max(1, z/threshold): all but the top `percentile` channels): x / 1 == x in
+// IEEE arithmetic for every finite x, so the division and the k / RN(1/k)
+// loads are skipped.
+template <bool kCheckX, bool kCheckK>
+__device__ __forceinline__ void smooth_chunk(const float (&x)[8], const float* __restrict__ kv,
+                                             const float* __restrict__ rkv, const uint8_t* __restrict__ kone, int c,
+                                             float (&q)[8]) {
+  if (kone && __ldg(kone + c)) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) q[t] = x[t];
+    return;
+  }
+  const int j = c * 8;
+  const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
+  const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
+  const float4 r0 = __ldg(reinterpret_cast<const float4*>(rkv + j));
+  const float4 r1 = __ldg(reinterpret_cast<const float4*>(rkv + j + 4));
+  const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+  const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+  div_chunk<kCheckX, kCheckK>(x, kk, rr, q);
+}
+
 template <int T, int V, int CL, bool kF16, bool kCheckK>
 __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
-                                                  const float* __restrict__ kv, const float* __restrict__ rkv, int K,
-                                                  int Kpad, int dynamic, float act_scale, int8_t* __restrict__ Q,
-                                                  size_t ldq, float* __restrict__ rs, int M) {
+                                                  const float* __restrict__ kv, const float* __restrict__ rkv,
+                                                  const uint8_t* __restrict__ kone, int K, int Kpad, int dynamic,
+                                                  float act_scale, int8_t* __restrict__ Q, size_t ldq,
+                                                  float* __restrict__ rs, int M) {
   __shared__ float red[33];
   __shared__ float cl_max;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -262,12 +287,6 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
     const int c = cbase + v * T;
     if (c < C8) {
       const int j = c * 8;
-      const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
-      const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
-      const float4 r0 = __ldg(reinterpret_cast<const float4*>(rkv + j));
-      const float4 r1 = __ldg(reinterpret_cast<const float4*>(rkv + j + 4));
-      const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-      const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
       float x[8];
       if constexpr (kF16) {
         const __half2* h2 = reinterpret_cast<const __half2*>(&raw[v][0]);
@@ -282,7 +301,7 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 #pragma unroll
         for (int t = 0; t < 8; ++t) x[t] = f[t];
       }
-      div_chunk<!kF16, kCheckK>(x, kk, rr, xv[v]);
+      smooth_chunk<!kF16, kCheckK>(x, kv, rkv, kone, c, xv[v]);
 #pragma unroll
       for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
     }
@@ -310,7 +329,10 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
     if (c < C8) {
       int o[8];
       if (safe) {
-        quant_chunk(xv[v], s, inv, o);
+        if (dynamic)
+          quant_chunk<false>(xv[v], s, inv, o);
+        else
+          quant_chunk<true>(xv[v], s, inv, o);
       } else {
 #pragma unroll
         for (int t = 0; t < 8; ++t) o[t] = quant_code_f64(xv[v][t], s);
@@ -328,9 +350,10 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 // previous row.  x' = x/k stays in registers between the absmax and the codes.
 template <int T, int V, bool kF16, bool kCheckK>
 __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
-                                                  const float* __restrict__ kv, const float* __restrict__ rkv, int K,
-                                                  int Kpad, int dynamic, float act_scale, int8_t* __restrict__ Q,
-                                                  size_t ldq, float* __restrict__ rs, int M) {
+                                                  const float* __restrict__ kv, const float* __restrict__ rkv,
+                                                  const uint8_t* __restrict__ kone, int K, int Kpad, int dynamic,
+                                                  float act_scale, int8_t* __restrict__ Q, size_t ldq,
+                                                  float* __restrict__ rs, int M) {
   extern __shared__ __align__(128) uint8_t sbuf[];
   __shared__ __align__(8) uint64_t full[2];
   __shared__ float red[33];
@@ -387,13 +410,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
           x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
           x[4] = bb.x; x[5] = bb.y; x[6] = bb.z; x[7] = bb.w;
         }
-        const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
-        const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
-        const float4 r0 = __ldg(reinterpret_cast<const float4*>(rkv + j));
-        const float4 r1 = __ldg(reinterpret_cast<const float4*>(rkv + j + 4));
-        const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-        const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        div_chunk<!kF16, kCheckK>(x, kk, rr, xv[v]);
+        smooth_chunk<!kF16, kCheckK>(x, kv, rkv, kone, c, xv[v]);
 #pragma unroll
         for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
       }
@@ -418,7 +435,10 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
       if (c < C8) {
         int o[8];
         if (safe) {
-          quant_chunk(xv[v], s, inv, o);
+          if (dynamic)
+            quant_chunk<false>(xv[v], s, inv, o);
+          else
+            quant_chunk<true>(xv[v], s, inv, o);
         } else {
 #pragma unroll
           for (int t = 0; t < 8; ++t) o[t] = quant_code_f64(xv[v][t], s);
@@ -499,9 +519,9 @@ cudaError_t dgq_launch_actquant_f16(const void* Xv, size_t ldx, int seg, size_t 
 
 namespace {
 template <int T, int V, int CL, bool F16, bool CK>
-cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, const float* rk, int K,
-                       int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq, float* rs, int M,
-                       cudaStream_t st) {
+cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, const float* rk,
+                       const uint8_t* kone, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
+                       float* rs, int M, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(M) * CL);
   cfg.blockDim = dim3(T);
@@ -513,14 +533,14 @@ cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, co
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = CL > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, CK>, X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,
-                            act_scale, Q, ldq, rs, M);
+  return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, CK>, X, ldx, seg, seg_stride, k, rk, kone, K, Kpad,
+                            dynamic, act_scale, Q, ldq, rs, M);
 }
 }  // namespace
 
 cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, size_t seg_stride, const float* k,
                                  const float* rk, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
-                                 float* rs, int M, cudaStream_t st, bool k_checked) {
+                                 float* rs, int M, cudaStream_t st, bool k_checked, const uint8_t* kone) {
   if (M <= 0) return cudaSuccess;
   if (seg <= 0) seg = K;
   const size_t align = f16 ? 8 : 4;  // elements per 16 bytes
@@ -555,7 +575,7 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     int occ = 1;                                                                                                \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, stage);                                       \
     const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \
-    kern<<<grid, T_, stage, st>>>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);  \
+    kern<<<grid, T_, stage, st>>>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);  \
     return cudaGetLastError();                                                                                  \
   }
     if (C8 <= 256) DGQ_AQ3(256, 1)
@@ -566,13 +586,13 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
 #undef DGQ_AQ3
   }
 #define DGQ_AQ(T_, V_, CL_)                                                                                    \
-  e = f16 ? (k_checked ? launch_aq2<T_, V_, CL_, true, false>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,    \
+  e = f16 ? (k_checked ? launch_aq2<T_, V_, CL_, true, false>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,    \
                                                                act_scale, Q, ldq, rs, M, st)                     \
-                       : launch_aq2<T_, V_, CL_, true, true>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,     \
+                       : launch_aq2<T_, V_, CL_, true, true>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,     \
                                                               act_scale, Q, ldq, rs, M, st))                     \
-          : (k_checked ? launch_aq2<T_, V_, CL_, false, false>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,   \
+          : (k_checked ? launch_aq2<T_, V_, CL_, false, false>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,   \
                                                                 act_scale, Q, ldq, rs, M, st)                    \
-                       : launch_aq2<T_, V_, CL_, false, true>(X, ldx, seg, seg_stride, k, rk, K, Kpad, dynamic,    \
+                       : launch_aq2<T_, V_, CL_, false, true>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,    \
                                                                act_scale, Q, ldq, rs, M, st))
   if (C8 <= 128) DGQ_AQ(128, 1, 1);
   else if (C8 <= 256) DGQ_AQ(128, 2, 1);

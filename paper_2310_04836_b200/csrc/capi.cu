@@ -125,6 +125,7 @@ struct dgq_layer {
   float* k = nullptr;        // [h]
   float* rk = nullptr;       // [h] RN(1/k): hoisted reciprocals for K1
   bool k_fast = false;       // every k <= 2^24: K1 skips the per-chunk k range check
+  uint8_t* kone = nullptr;   // [h/8] chunk c's eight k are all exactly 1 (K1 skips their division)
   size_t device_bytes = 0;
   CUtensorMap tmA{};  // non-fused A operand
   std::mutex ws_mu;
@@ -244,6 +245,7 @@ void dgq_layer_destroy(dgq_layer* L) {
   cudaFree(L->s1);
   cudaFree(L->k);
   cudaFree(L->rk);
+  cudaFree(L->kone);
   cudaFree(L->ws);
   cudaSetDevice(prev);
   delete L;
@@ -315,6 +317,16 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
   L->k_fast = true;
   for (size_t j = 0; j < h; ++j) L->k_fast = L->k_fast && k[j] <= 0x1p24f;
   DGQ_CUDA_L(dgq_launch_reciprocal(L->k, L->rk, static_cast<int>(h), st));
+  if (h % 8 == 0) {
+    std::vector<uint8_t> kone(h / 8);
+    for (size_t c = 0; c < h / 8; ++c) {
+      bool one = true;
+      for (size_t t = 0; t < 8; ++t) one = one && k[c * 8 + t] == 1.0f;
+      kone[c] = one ? 1 : 0;
+    }
+    DGQ_CUDA_L(cudaMalloc(&L->kone, h / 8));
+    DGQ_CUDA_L(cudaMemcpy(L->kone, kone.data(), h / 8, cudaMemcpyHostToDevice));
+  }
   L->device_bytes = (L->o + h) * sizeof(float);
   if (L->fused) {
     const size_t tb = static_cast<size_t>(L->n_tiles) * L->k_blocks * dgq_layout::chunk_bytes(static_cast<int>(g));
@@ -469,7 +481,7 @@ dgq_status dgq_quantize_act_f16(const dgq_layer* L, const void* dX, size_t M, si
   if (seg_cols && seg_stride < M * ldx) return fail(DGQ_EINVAL, "seg_stride smaller than one shard");
   DGQ_CUDA(dgq_launch_actquant2(dX, true, ldx, static_cast<int>(seg), seg_stride, L->k, L->rk,
                                 static_cast<int>(L->h), static_cast<int>(ldq), L->mode, L->act_scale, dXq, ldq,
-                                dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast));
+                                dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast, L->kone));
   return DGQ_OK;
 }
 
@@ -482,7 +494,7 @@ dgq_status dgq_quantize_act(const dgq_layer* L, const float* dX, size_t M, size_
   if (M > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too many rows");
   DGQ_CUDA(dgq_launch_actquant2(dX, false, ldx, static_cast<int>(L->h), 0, L->k, L->rk, static_cast<int>(L->h),
                                 static_cast<int>(ldq), L->mode, L->act_scale, dXq, ldq, dRowScale,
-                                static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast));
+                                static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast, L->kone));
   return DGQ_OK;
 }
 

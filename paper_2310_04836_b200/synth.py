@@ -63,6 +63,34 @@ def gen_synthetic(rows: int, cols: int, seed: int, count: int = 0, magnitude: fl
     return v
 
 
+def channel_maxima(calib) -> np.ndarray:
+    """max |x| per channel over a calibration set (proj/src/smoothing.cpp:9-24)."""
+    z = None
+    for t in calib:
+        m = np.max(np.abs(np.asarray(t, np.float32)), axis=0)
+        z = m if z is None else np.maximum(z, m)
+    return z.astype(np.float32)
+
+
+def compute_smooth(z, percentile: float) -> np.ndarray:
+    """k = max(1, z / threshold), threshold = the ceil(percentile * h)-th largest
+    channel maximum (proj/src/smoothing.cpp:26-49): k is exactly 1 on all but
+    the top `percentile` of the channels."""
+    z = np.asarray(z, np.float32)
+    rank = max(int(np.ceil(np.float64(np.float32(percentile)) * z.size)), 1)
+    thr = np.sort(z)[::-1][rank - 1]
+    if not thr > 0:
+        raise ValueError("smoothing undefined: percentile threshold is not positive")
+    return np.maximum(np.float32(1.0), (z / thr).astype(np.float32)).astype(np.float32)
+
+
+def smooth_k(h: int, seed: int = 100, percentile: float = 0.005) -> np.ndarray:
+    """The smoothing vector of SURVEY.md §8d: compute_smooth over the channel
+    maxima of 256 synthetic calibration rows with the standard outlier spec
+    (3 channels x 50, column seed 7; proj/manifests/standard_suite.json:7)."""
+    return compute_smooth(channel_maxima([gen_synthetic(256, h, seed, 3, 50.0, 7)]), percentile)
+
+
 def pack_u4(vals) -> np.ndarray:
     """Nibble packing, even index in the LOW nibble (proj/src/tensor.cpp:124-132)."""
     v = np.asarray(vals, np.uint8).ravel()

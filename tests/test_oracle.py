@@ -165,3 +165,16 @@ def test_validation_fields_match_ref(port, ref, field, mutate):
     with pytest.raises(oracle.OracleError) as e2:
         port.validate_layer(L)
     assert e1.value.field == field and e2.value.field == field
+
+
+@pytest.mark.parametrize("h", [65, 7168])
+def test_bench_smoothing_vector_is_the_references(port, ref, h):
+    # bench.py's k (synth.smooth_k) = the reference's compute_smooth over the
+    # channel maxima of its own synthetic calibration rows
+    from paper_2310_04836_b200 import synth
+
+    X = ref.gen_synthetic(256, h, 100, 3, 50.0, 7)
+    k_ref, _ = ref.smooth_from_calib(X, 0.005)
+    assert np.array_equal(synth.smooth_k(h).view(np.uint32), k_ref.view(np.uint32))
+    if h == 7168:  # the K1 unit-k fast path covers most chunks
+        assert (k_ref.reshape(-1, 8) == 1.0).all(axis=1).mean() > 0.9

@@ -147,6 +147,30 @@ def test_actq_random(cuda, port, M, K, mode):
     assert np.array_equal(bits(aq.row_scales), bits(rs))
 
 
+@pytest.mark.parametrize("M,K,mode,f16", [(1, 7168, 1, False), (16, 28672, 1, True), (300, 7168, 1, False),
+                                          (2048, 7168, 1, False), (512, 28672, 1, True), (200, 4096, 0, False),
+                                          (333, 4096, 0, True)])
+def test_actq_smoothing_vector_with_unit_chunks(cuda, port, M, K, mode, f16):
+    # k from the reference's compute_smooth recipe: exactly 1 on ~96 % of the
+    # 8-channel chunks (K1 skips their division) and > 1 on the outliers
+    from paper_2310_04836_b200 import synth
+
+    k = synth.smooth_k(K)
+    k[5] = 1.0 + 2.0 ** -23  # a chunk with one k just above 1 takes the division
+    X = port.gen_synthetic(M, K, 77 + M, 3, 50.0, 7)
+    if f16:
+        X = X.astype(np.float16).astype(np.float32)
+    act = float(np.abs(X / k).max() / 127.0 * 0.8)
+    q, rs = port.quantize_activations(X, k, mode, act)
+    L = dgq.DgqLayer(h=K, o=2, g=K // 8, codes=np.zeros(K, np.uint8), s2=np.ones((8, 2), np.int8),
+                     zp=np.zeros(8, np.uint8), s1=np.ones(2, np.float32), k=k, act_scale=act, mode=mode)
+    CL = dgq.CudaLayer(L)
+    x = torch.from_numpy(X).cuda()
+    codes, drs = CL.quantize_act(x.half() if f16 else x)
+    assert np.array_equal(codes[:, :K].cpu().numpy(), q)
+    assert np.array_equal(bits(drs.cpu().numpy()), bits(rs))
+
+
 def test_actq_ties_exhaustive(cuda, port):
     # every half-integer quotient (n + 1/2) * s for a spread of scales: ties must go to even
     rows = []

@@ -14,6 +14,9 @@ import paper_2310_04836_b200 as dgq  # noqa: E402
 M, K, N = (int(v) for v in sys.argv[1:4])
 copies = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 lib = dgq.lib()
+lib.dgq_debug_set_decode.argtypes = [C.c_int]
+if len(sys.argv) > 5:
+    lib.dgq_debug_set_decode(int(sys.argv[5], 0))
 lib.dgq_debug_set_timestamps.argtypes = [C.c_void_p]
 base = dgq.random_layer(K, N, 128, seed=3)
 layers = [dgq.CudaLayer(base, validate=False) for _ in range(copies)]
@@ -38,9 +41,17 @@ torch.cuda.synchronize()
 g.replay()
 torch.cuda.synchronize()
 st = [b.view(16, 1024)[14].cpu().numpy() for b in bufs]
+sm = [b.view(16, 1024)[13][512:].cpu().numpy() for b in bufs]
 en = [b.view(16, 1024)[15].cpu().numpy() for b in bufs]
 t0 = min(x[x > 0].min() for x in st)
 for i in range(n):
     a, b = st[i][st[i] > 0], en[i][en[i] > 0]
     print(f"launch {i}: CTA start {(a.min() - t0) / 1e3:7.2f}..{(a.max() - t0) / 1e3:7.2f}  "
           f"end {(b.min() - t0) / 1e3:7.2f}..{(b.max() - t0) / 1e3:7.2f} us")
+# per SM: next launch's CTA start - this launch's CTA end on the same SM
+for i in range(n - 1):
+    ends = {int(sm[i][c]): en[i][c] for c in range(min(512, len(en[i]))) if en[i][c] > 0}
+    d = [(st[i + 1][c] - ends[int(sm[i + 1][c])]) / 1e3 for c in range(min(512, len(st[i + 1])))
+         if st[i + 1][c] > 0 and int(sm[i + 1][c]) in ends]
+    if d:
+        print(f"launch {i}->{i + 1}: same-SM end->start gap min {min(d):.2f} median {np.median(d):.2f} max {max(d):.2f} us")

@@ -24,9 +24,9 @@ int main() {
   cudaStream_t st; cudaStreamCreate(&st);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int tm : {0, 1})
-  for (int smem : {190 * 1024})
-    for (int thr : {512}) for (int pdl : {0, 1}) {
-      cudaFuncSetAttribute(k_spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  for (int smem : {0, 48 * 1024, 190 * 1024})
+    for (int thr : {128, 512}) for (int pdl : {0, 1}) {
+      cudaFuncSetAttribute(k_spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaGraph_t g; cudaGraphExec_t ge;
       cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
       const int n = 20;
