@@ -568,9 +568,12 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
   DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), static_cast<int>(N), static_cast<int>(k_pad), fused, g);
   if (pl.ws_bytes + pl.counter_bytes > ws_bytes)
     return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(pl.ws_bytes + pl.counter_bytes));
-  CUtensorMap tmB;
-  dgq_status ms = make_tmap(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn));
-  if (ms != DGQ_OK) return ms;
+  CUtensorMap tmB{};
+  dgq_status ms = DGQ_OK;
+  if (!pl.prefill2) {  // K5p builds its own 128-row map below
+    ms = make_tmap(&tmB, dXq, M, k_pad, ldq, static_cast<uint32_t>(pl.bn));
+    if (ms != DGQ_OK) return ms;
+  }
   if (pl.decode) {
     if (!ws) return fail(DGQ_EINVAL, "decode kernel needs a workspace");
     DecodeSub one{tiles, dS1, dBias, dY, ldy, static_cast<int>(N)};
@@ -618,13 +621,14 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     ms = make_tmap(&tmX, dXq, M, k_pad, ldq, 128u);
     if (ms != DGQ_OK) return ms;
     p.chunk_stride = p.chunk_bytes;
+    p.dbg_flags = (dgq_debug_decode_mode() >> 18) & 7;  // tools: mode bits 18-20
     if (pl.stream_k) {
       if (!ws) return fail(DGQ_EINVAL, "stream-K prefill kernel needs a workspace");
       p.stream_k = 1;
       p.ws = static_cast<int32_t*>(ws);
       p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
     }
-    DGQ_CUDA(dgq_launch_prefill2(tmX, tmY, p, pl.pair_tn, pl.pdl != 0, st));
+    DGQ_CUDA(dgq_launch_prefill2(tmX, tmY, p, pl.pair_tn, pl.pair_sub, pl.pdl != 0, st));
     return DGQ_OK;
   }
   DGQ_CUDA(dgq_launch_gemm(pl, fused, tmB, tmA, tmY, p, st));

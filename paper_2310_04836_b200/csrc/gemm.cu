@@ -578,10 +578,11 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
   // bit 12 disables K5p, bit 13 disables stream-K (round-robin whole tiles,
   // and then K5p only when its tiles fill >= 6 waves of pairs).
   const bool sk = (g_decode_mode & 0x2000) == 0;
+  const uint32_t cb = static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128));
   const long long t256_ = static_cast<long long>((M + 255) / 256) * ((N + 255) / 256);
   const bool pair_ok = (g_decode_mode & 0x400) != 0 || sk || t256_ >= 6LL * (sm_count() / 2);
   if (fused && M >= 256 && pair_ok && (g_decode_mode & 0x1000) == 0 && !force_bn && !force_splits &&
-      dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128))) <= 232448) {
+      dgq_prefill2_smem_bytes(cb, 1) <= 232448) {
     const int pairs = sm_count() / 2;
     const long long mp = (M + 255) / 256;
     const long long t256 = mp * ((N + 255) / 256), t128 = mp * ((N + 127) / 128);
@@ -592,14 +593,18 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
     // round robin: the 128-wide tile measured ~40 % slower per tile area, so it
     // is only taken when it saves more than half of the 256-wide tail
     pl.pair_tn = ((g_decode_mode & 0x800) != 0 || (!sk && c128 * 1.6 < c256)) ? 128 : 256;
-    pl.bn = 256;
+    // two token sub-tiles per CTA (512-token pair tiles) from 512 tokens, with
+    // stream-K balancing the tiles; mode bit 17 keeps one (256-token tiles)
+    pl.pair_sub = (sk && pl.pair_tn == 256 && M >= 512 && (g_decode_mode & 0x20000) == 0 &&
+                   dgq_prefill2_smem_bytes(cb, 2) <= 232448) ? 2 : 1;
+    pl.bn = 256 * pl.pair_sub;
     pl.nt = pl.pair_tn / 128;
-    pl.m_tiles = static_cast<int>(mp);
+    pl.m_tiles = static_cast<int>((M + pl.bn - 1) / pl.bn);
     pl.n_tiles = (N + 127) / 128;
     pl.splits = 1;
     pl.kb_per_split = kblocks;
-    pl.ctas = 2 * dgq_prefill2_clusters(M, N, pl.pair_tn, kblocks, sk);
-    pl.smem_bytes = dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128)));
+    pl.ctas = 2 * dgq_prefill2_clusters(M, N, pl.pair_tn, kblocks, sk, pl.pair_sub);
+    pl.smem_bytes = dgq_prefill2_smem_bytes(cb, pl.pair_sub);
     if (sk) {
       pl.ws_bytes = static_cast<size_t>(pairs) * kPrefill2SlotBytes;
       pl.counter_bytes = static_cast<size_t>(pairs) * 2 * 4;

@@ -58,6 +58,7 @@ struct DgqGemmParams {
   uint32_t* counters;
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
   int stream_k;             // K5p: stream-K over (tile, k-block) units (ws / counters = pair slots / flags)
+  int dbg_flags;            // tools only (K5p): 1 = epilogue skips its global stores, 2 = also its math, 4 = math only
 };
 
 // K5d (decode.cu): stream-K over (weight tile, k-block) units, (code - ZP) as
@@ -111,6 +112,7 @@ struct DgqGemmPlan {
   int prefill2;  // 1: K5p (prefill.cu), persistent CTA pairs, 256 x `pair_tn` tiles
   int pair_tn;   // 256 or 128 channels per pair tile
   int stream_k;  // K5p: stream-K work split (workspace = ws_bytes + counter_bytes)
+  int pair_sub;  // K5p: token sub-tiles per CTA (pair tile = 256 * pair_sub tokens)
   int ctas;
   int bn;
   int nt;  // 128-row weight tiles per CTA
@@ -125,12 +127,13 @@ struct DgqGemmPlan {
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn = 0, int force_splits = 0);
 
 // K5p (prefill.cu): persistent CTA-pair kernel; tmA = Xq with 128-row boxes.
-size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride);
-int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k);
-// stream-K workspace: per pair two CTA partials of 128 x 256 int32, + flags
-constexpr size_t kPrefill2SlotBytes = 2 * 128 * 256 * 4;
+// sub = token sub-tiles per CTA (1: 256-token pair tiles, 2: 512-token pair tiles)
+size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride, int sub);
+int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int sub);
+// stream-K workspace: per pair two CTA partials of up to 2 x 128 x 256 int32, + flags
+constexpr size_t kPrefill2SlotBytes = 2 * 2 * 128 * 256 * 4;
 cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,
-                                bool pdl, cudaStream_t st);
+                                int sub, bool pdl, cudaStream_t st);
 
 cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorMap& tmB, const CUtensorMap& tmA,
                             const CUtensorMap& tmY, const DgqGemmParams& p, cudaStream_t st);

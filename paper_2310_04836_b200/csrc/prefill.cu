@@ -46,17 +46,28 @@ namespace pf {
 // lands ~0.5-0.8 us after issue and a group dequantises a k-block in ~0.8 us,
 // against a 0.26 us MMA step, so the packed chunks are fetched kLag k-blocks
 // ahead of the Xq tiles and released by the dequantisers (not the MMA).
-constexpr int kSA = 5;            // Xq tile stages (released by the MMA)
-constexpr int kSC = 7;            // packed-chunk stages (released by the dequantisers)
-constexpr int kLag = kSC - kSA;   // chunk i is issued together with Xq tile i - kLag
-constexpr int kSB = 4;            // dequantised weight-tile slots (> dequant groups: a group can run ahead)
-constexpr int kDqGroups = 3;      // groups of four dequant warps, alternate k-blocks
-constexpr int kEpiWarp0 = 4 + 4 * kDqGroups;  // first of the four epilogue warps
-constexpr int kXWarp = kEpiWarp0 + 4;         // second Xq-tile producer warp
-constexpr int kThreads = 32 * (kXWarp + 1);
+// S = token sub-tiles per CTA: each dequantised weight tile feeds S MMAs
+// (pair tile = 256*S tokens x TN channels), so the INT4 -> INT8 work per MMA
+// cycle falls by S.  S = 2 fills TMEM with one accumulator set (2 x 256
+// columns): the epilogue of a tile no longer overlaps the next tile's main
+// loop, but the dequantisers (now two groups) have twice the time per k-block.
+template <int S>
+struct Cfg {
+  static constexpr int kSA = S == 1 ? 5 : 3;        // Xq stages (S tiles each, released by the MMA)
+  static constexpr int kSC = S == 1 ? 7 : 5;        // packed-chunk stages (released by the dequantisers)
+  static constexpr int kSB = S == 1 ? 4 : 3;        // dequantised weight-tile slots (> dequant groups)
+  static constexpr int kDqGroups = S == 1 ? 3 : 2;  // groups of four dequant warps, alternate k-blocks
+  static constexpr int kEpiWarp0 = 4 + 4 * kDqGroups;  // first epilogue warp
+  // S == 2 exposes the epilogue (one accumulator set): two warps per TMEM lane
+  // quadrant split the channels
+  static constexpr int kEpiWarps = S == 1 ? 4 : 8;
+  static constexpr int kXWarp = kEpiWarp0 + kEpiWarps;  // second Xq-tile producer warp
+  static constexpr int kThreads = 32 * (kXWarp + 1);
+  static constexpr int kNAcc = 2 / S;               // accumulator sets in TMEM (256 * S columns each)
+};
 constexpr uint32_t kATile = 128 * 128;   // 128 token rows x 128 k (bytes)
 constexpr uint32_t kBTile = 128 * 128;   // 128 channel rows x 128 k
-constexpr uint32_t kStaging = 4 * 4096;  // epilogue: one 4 KB staging buffer per epilogue warp
+constexpr uint32_t kStagingPerWarp = 4096;  // epilogue: one 4 KB staging buffer per epilogue warp
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -268,20 +279,137 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* a) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
   return v;
 }
-// r[0..15] += the contributors' partials of 16 columns (chunk c16 of this
-// thread's row).  part: first contributor's slot + row offset; pstride: ints
-// between consecutive pairs' slots.  Layout per slot: [c16][row][16] int32.
-__device__ __forceinline__ void add_partials16(uint32_t* r, const int32_t* part, int npart, size_t pstride, int c16) {
-  for (int pi = 0; pi < npart; ++pi) {
-    const int4* s = reinterpret_cast<const int4*>(part + pi * pstride + static_cast<size_t>(c16) * 2048);
+// Stream-K partial layout (one 128-row sub-tile, 128 KB): [c16][v][row][4]
+// int32 — chunk c16 of 16 columns, quarter v of it, token row, 4 values — so
+// a warp's 16-byte stores and loads of one (c16, v) are 512 contiguous bytes.
+__device__ __forceinline__ size_t part_off(int c16, int v, int row) {
+  return (static_cast<size_t>(c16 * 4 + v) * 128 + row) * 4;
+}
+
+// Exposed epilogue of the two-sub-tile kernel: 32 token rows (this warp's
+// TMEM lane quadrant) x TN channels -> scales -> FP16/FP32, transposed through
+// the warp's 4 KB staging buffer so each global store instruction writes four
+// whole 128-byte row segments (a lane-per-row 16-byte store touched 32 lines
+// per instruction; tools/pf_trace.py measured an 11 us epilogue that way, and
+// a TMA store per 64 columns serialises on its issue latency).
+template <int TN, bool kF16>
+__device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbase, float rsm, const float* s_s1,
+                                           const float* s_bias, uint8_t* stg, int mrow0, int nbase, int cbeg,
+                                           int cend) {
+  // the FP16 epilogue mode and the bias are uniform runtime branches: every
+  // template variant unrolled here cost instruction-cache misses (the kernel's
+  // SASS reached 350 KB and the exposed epilogue ran at ~1/6 of its issue rate)
+  const bool kF16Mode = p.fp16_mode != 0, kBias = p.bias != nullptr;
+  constexpr int kCB = kF16 ? 64 : 32;  // columns per 128-byte row segment
+  const uint32_t lane = lane_id();
+  uint8_t* myrow = stg + lane * 128;
+  const uint32_t sw = lane & 7;
+#pragma unroll 1
+  for (int c0 = cbeg; c0 < cend; c0 += kCB) {
+    if (nbase + c0 >= p.N) break;
+    // 16-column TMEM loads, the next one in flight while this one is converted
+    // (a whole 64-column batch in registers spilled: 96 registers per thread)
+    uint32_t r[2][16];
+    tmem_ld16(tbase + c0, r[0]);
+    tmem_ld_wait();
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int4 x = __ldcg(s + v);
-      r[4 * v + 0] += static_cast<uint32_t>(x.x);
-      r[4 * v + 1] += static_cast<uint32_t>(x.y);
-      r[4 * v + 2] += static_cast<uint32_t>(x.z);
-      r[4 * v + 3] += static_cast<uint32_t>(x.w);
+    for (int c16 = 0; c16 < kCB; c16 += 16) {
+      uint32_t (&cur)[16] = r[(c16 / 16) & 1];
+      if (c16 + 16 < kCB) tmem_ld16(tbase + c0 + c16 + 16, r[((c16 / 16) + 1) & 1]);
+      if (!(p.dbg_flags & 2)) {
+#pragma unroll
+        for (int c8 = 0; c8 < 16; c8 += 8) {
+          const int c1 = c16 + c8;
+          float y[8];
+          const float4 sa = *reinterpret_cast<const float4*>(s_s1 + c0 + c1);
+          const float4 sb = *reinterpret_cast<const float4*>(s_s1 + c0 + c1 + 4);
+          const float sv[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+          bool small = true;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            bool ok;
+            y[k] = i2f_small(static_cast<int32_t>(cur[c8 + k]), ok);
+            small &= ok;
+          }
+          if (!__all_sync(0xffffffffu, small)) {  // some |acc| >= 2^22: the exact conversion
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = __int2float_rn(static_cast<int32_t>(cur[c8 + k]));
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) y[k] = __fmul_rn(__fmul_rn(y[k], rsm), sv[k]);
+          if (kF16Mode) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = epilogue_f16mode(static_cast<int32_t>(cur[c8 + k]), rsm, sv[k]);
+          }
+          if (kBias) {
+            const float4 ba = *reinterpret_cast<const float4*>(s_bias + c0 + c1);
+            const float4 bb = *reinterpret_cast<const float4*>(s_bias + c0 + c1 + 4);
+            y[0] = __fadd_rn(y[0], ba.x); y[1] = __fadd_rn(y[1], ba.y); y[2] = __fadd_rn(y[2], ba.z);
+            y[3] = __fadd_rn(y[3], ba.w); y[4] = __fadd_rn(y[4], bb.x); y[5] = __fadd_rn(y[5], bb.y);
+            y[6] = __fadd_rn(y[6], bb.z); y[7] = __fadd_rn(y[7], bb.w);
+          }
+          if (kF16) {
+            uint32_t h[4];
+            uint32_t tiny = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const __half2 hh = __floats2half2_rn(y[2 * k], y[2 * k + 1]);
+              h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+              // IEEE rounding differs from fp16_round (proj/src/quant.cpp:33-35,
+              // |x| < 2^-24 -> signed zero) only where it produced +-2^-24 (0x0001)
+              tiny |= static_cast<uint32_t>((h[k] & 0x7FFFu) == 1u) |
+                      static_cast<uint32_t>((h[k] & 0x7FFF0000u) == 0x10000u);
+            }
+            if (tiny) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                uint32_t u = h[k];
+                if (fabsf(y[2 * k]) < 0x1p-24f) u = (u & 0xFFFF0000u) | ((__float_as_uint(y[2 * k]) >> 16) & 0x8000u);
+                if (fabsf(y[2 * k + 1]) < 0x1p-24f)
+                  u = (u & 0x0000FFFFu) | (__float_as_uint(y[2 * k + 1]) & 0x80000000u);
+                h[k] = u;
+              }
+            }
+            if (p.dbg_flags & 4) {  // tools: math only (no staging)
+              if ((h[0] ^ h[1] ^ h[2] ^ h[3]) == 0x12345678u) *static_cast<uint32_t*>(p.out) = h[0];
+            } else {
+              *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
+            }
+          } else {
+            *reinterpret_cast<float4*>(myrow + (((c1 / 4) ^ sw) << 4)) = make_float4(y[0], y[1], y[2], y[3]);
+            *reinterpret_cast<float4*>(myrow + (((c1 / 4 + 1) ^ sw) << 4)) = make_float4(y[4], y[5], y[6], y[7]);
+          }
+        }
+      }
+      if (c16 + 16 < kCB) tmem_ld_wait();
     }
+    if (p.dbg_flags & 6) continue;
+    __syncwarp();
+    // 8 passes x (4 rows x 8 lanes x 16 bytes)
+    const int ch = static_cast<int>(lane & 7);                 // 16-byte chunk of the row segment
+    const int n = nbase + c0 + ch * (kF16 ? 8 : 4);            // first output column of the chunk
+    constexpr int kPer = kF16 ? 8 : 4;                         // outputs per chunk
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int row = it * 4 + static_cast<int>(lane >> 3);
+      const int m = mrow0 + row;
+      const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
+      if (m < p.M && !(p.dbg_flags & 1)) {
+        uint8_t* dst = static_cast<uint8_t*>(p.out) + (static_cast<size_t>(m) * p.ldy + n) * (kF16 ? 2 : 4);
+        if (n + kPer <= p.N) {
+          *reinterpret_cast<uint4*>(dst) = v;
+        } else if (n < p.N) {
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          for (int k = 0; k < kPer && n + k < p.N; ++k) {
+            if (kF16)
+              reinterpret_cast<uint16_t*>(dst)[k] = static_cast<uint16_t>(w[k >> 1] >> ((k & 1) * 16));
+            else
+              reinterpret_cast<uint32_t*>(dst)[k] = w[k];
+          }
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -348,25 +476,32 @@ __device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase,
 // rows, one prepared tile) or 128 (each CTA dequantises 64 rows of the SAME
 // prepared tile; twice the tiles, for shapes whose 256-wide tiles leave a
 // ragged last wave).
-template <int TN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
+template <int TN, int S>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads, 1)
     k_dgq_prefill2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
                    const DgqGemmParams p) {
   using namespace pf;
+  using C = Cfg<S>;
+  constexpr int kSA = C::kSA, kSC = C::kSC, kSB = C::kSB, kDqGroups = C::kDqGroups;
+  constexpr int kEpiWarp0 = C::kEpiWarp0, kXWarp = C::kXWarp, kNAcc = C::kNAcc, kEpiWarps = C::kEpiWarps;
+  constexpr int kEpiThreads = 32 * kEpiWarps;
+  constexpr uint32_t kStaging = kEpiWarps * kStagingPerWarp;
+  constexpr uint32_t kAStage = S * kATile;  // one Xq stage: S tiles of 128 token rows
+  static_assert(S == 1 || TN == 256, "two token sub-tiles use the 256-wide pair tile");
   constexpr uint32_t kIdesc = idesc_i8(256, TN);
   constexpr int kRows = TN / 2;  // channel rows of B held (and dequantised) by each CTA
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int KB = p.k_blocks;
   const int n_tiles = (p.N + 127) / 128;  // 128-channel weight tiles (prepared chunks)
-  const int m_pairs = (p.M + 255) / 256, n_pairs = (p.N + TN - 1) / TN;
+  const int m_pairs = (p.M + 256 * S - 1) / (256 * S), n_pairs = (p.N + TN - 1) / TN;
   const int total = m_pairs * n_pairs;
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = sm;                          // [kSA][128 x 128] Xq (SW128 K-major)
-  uint8_t* sB = sA + kSA * kATile;           // [kSB][128 x 128] W_s8 (SW128 K-major)
+  uint8_t* sA = sm;                          // [kSA][S][128 x 128] Xq (SW128 K-major)
+  uint8_t* sB = sA + kSA * kAStage;          // [kSB][128 x 128] W_s8 (SW128 K-major)
   uint8_t* sStg = sB + kSB * kBTile;         // epilogue staging
   uint8_t* sC = sStg + kStaging;             // [kSC][chunk_stride] packed chunks
   uint64_t* bars = reinterpret_cast<uint64_t*>(sC + kSC * p.chunk_stride);
@@ -376,11 +511,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
   uint64_t* cempty = cfull + kSC;            // [kSC] dequantised (one arrive by the group)
   uint64_t* ready = cempty + kSC;            // [kSB] leader: both CTAs' B slot dequantised (2 arrivals)
   uint64_t* bempty = ready + kSB;            // [kSB] MMA done with the B slot (multicast commit)
-  uint64_t* tfull = bempty + kSB;            // [2] accumulator complete (multicast commit)
+  uint64_t* tfull = bempty + kSB;            // [2] accumulator set complete (multicast commit)
   uint64_t* tempty = tfull + 2;              // [2] leader: both CTAs' epilogues drained it (8 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* s_rs = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
-  float* s_s1 = s_rs + 128;                                // [TN]
+  uint64_t* fbar = tempty + 2;               // [1] stream-K fix-up: a contributor's partial landed in sA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fbar + 1);
+  // 16-byte aligned (float4 reads) by an offset, so the pointer stays in the shared window (LDS, not generic LD)
+  uint8_t* after_slot = reinterpret_cast<uint8_t*>(tmem_slot + 4);
+  float* s_rs = reinterpret_cast<float*>(after_slot + ((16u - (smem_u32(after_slot) & 15u)) & 15u));  // [S * 128]
+  float* s_s1 = s_rs + 128 * S;                            // [TN]
   float* s_bias = s_s1 + 256;                              // [TN]
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -399,11 +537,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
     }
+    mbar_init(fbar, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmY);
+  }
+  if (p.dbg && threadIdx.x == 0 && blockIdx.x < 1024) {  // tools/pf_trace.py: CTA start
+    uint64_t g;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+    p.dbg[7 * 1024 + blockIdx.x] = g;
   }
   if (warp == 1) tmem_alloc2<512>(tmem_slot);
   tc_fence_before();
@@ -461,12 +605,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         si.advance(c);
         const int s = i % kSA;
         wait_local(&aempty[s], ((i / kSA) & 1) ^ 1, 7);
-        const int mpair = (t % m_pairs) * 256;
-        // a token half entirely past M is not loaded: its rows of D are never stored
-        if (leader)
-          mbar_arrive_expect_tx(&afull[s], (mpair < p.M ? kATile : 0u) + (mpair + 128 < p.M ? kATile : 0u));
-        const int mrow = mpair + static_cast<int>(rank) * 128;
-        if (mrow < p.M) tma_load_2d_pair(sA + s * kATile, &tmA, afull_leader + s * 8, kb * 128, mrow);
+        const int mpair = (t % m_pairs) * 256 * S;
+        // token quarters entirely past M are not loaded: their rows of D are never stored
+        if (leader) {
+          uint32_t tx = 0;
+#pragma unroll
+          for (int q = 0; q < 2 * S; ++q) tx += mpair + q * 128 < p.M ? kATile : 0u;
+          mbar_arrive_expect_tx(&afull[s], tx);
+        }
+#pragma unroll
+        for (int sub = 0; sub < S; ++sub) {
+          const int mrow = mpair + sub * 256 + static_cast<int>(rank) * 128;
+          if (mrow < p.M)
+            tma_load_2d_pair(sA + s * kAStage + sub * kATile, &tmA, afull_leader + s * 8, kb * 128, mrow);
+        }
         pf_stamp(p, 5, i);
       }
     }
@@ -479,10 +631,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
       SegIter si(p, cid, ncl, total, KB);
       int t, lo, hi;
       for (; si.next(t, lo, hi); ++tl) {
-        const int acc = tl & 1;
-        wait_cluster(&tempty[acc], ((tl >> 1) & 1) ^ 1, 2);  // both epilogues drained this accumulator
+        const int acc = tl % kNAcc;
+        {  // both epilogues drained this accumulator set; back off while polling so the
+           // spinning issuer does not take the issue slots of the epilogue warp
+           // sharing its SMSP (the epilogue is exposed when S == 2)
+          long long n = 0;
+          while (!try_wait_cluster(&tempty[acc], ((tl / kNAcc) & 1) ^ 1)) {
+            __nanosleep(128);
+            watchdog(n, 2, 0);
+          }
+        }
         tc_fence_after();
-        const uint32_t d = tm + acc * 256;  // accumulator slot (TN <= 256 columns)
+        const uint32_t d = tm + acc * 256 * S;  // accumulator set: S x (TN <= 256) columns
         for (int kb = lo; kb < hi; ++kb, ++it) {
           const int s = it % kSA, b = it % kSB;
           wait_cluster(&ready[b], (it / kSB) & 1, 3);  // both CTAs' B slots dequantised
@@ -493,10 +653,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
             p.dbg[it] = g;
           }
           tc_fence_after();
-          const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kATile));
           const uint64_t db = umma_desc_sw128(smem_u32(sB + b * kBTile));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) mma2_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb != lo) || kk != 0);
+          for (int sub = 0; sub < S; ++sub) {
+            const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kAStage + sub * kATile));
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma2_i8(d + sub * 256, da + 2 * kk, db + 2 * kk, kIdesc, (kb != lo) || kk != 0);
+          }
           commit2_mc(&aempty[s]);
           commit2_mc(&bempty[b]);
         }
@@ -579,44 +743,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
     }
   } else if (warp >= static_cast<uint32_t>(kEpiWarp0) && warp < static_cast<uint32_t>(kXWarp)) {
     // ------------------------------ epilogue ------------------------------
-    const int e = threadIdx.x - 32 * kEpiWarp0;      // 0..127 = token row of this CTA's D
+    const int et = threadIdx.x - 32 * kEpiWarp0;     // 0 .. kEpiThreads-1
     const uint32_t q = warp & 3;                     // TMEM lane quadrant
+    const int e = static_cast<int>(q * 32 + lane);   // token row of this CTA's D
+    constexpr int kCols = TN / (kEpiWarps / 4);       // channels per warp
+    const int cbeg = ((warp - kEpiWarp0) >> 2) * kCols, cend = cbeg + kCols;
     const uint32_t tempty_leader = mapa(tempty, 0);
-    uint8_t* stg0 = sStg + (warp - kEpiWarp0) * 4096;
+    uint8_t* stg0 = sStg + (warp - kEpiWarp0) * kStagingPerWarp;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // row scales from K1
     int tl = 0;
     SegIter si(p, cid, ncl, total, KB);
     const long long U = static_cast<long long>(total) * KB;
-    constexpr size_t kSlot = 128 * TN;  // ints per CTA partial
-    const size_t pstride = 2 * kSlot;   // ints between pairs' slots
+    constexpr size_t kSub = 128 * TN;    // ints of one 128-row partial
+    constexpr size_t kSlot = S * kSub;   // ints per CTA partial (S sub-tiles)
+    const bool b_ = p.bias != nullptr, f_ = p.fp16_mode != 0;
+    uint32_t fphase = 0;
     int t, lo, hi;
     for (; si.next(t, lo, hi); ++tl) {
       const int mt = t % m_pairs, nt = t / m_pairs;
-      const int acc = tl & 1;
-      const int m0 = mt * 256 + static_cast<int>(rank) * 128;
+      const int acc = tl % kNAcc;
+      const uint32_t tpar = (tl / kNAcc) & 1;
       const int n0 = nt * TN;
-      const uint32_t tbase = tmem + ((q * 32) << 16) + acc * 256;
       const int mrow = q * 32 + lane;
+      // sub-tile `sub` of this CTA: token rows mt*256S + sub*256 + rank*128 + [0, 128)
+      auto m0_of = [&](int sub) { return mt * 256 * S + sub * 256 + static_cast<int>(rank) * 128; };
+      auto tbase_of = [&](int sub) {
+        return tmem + ((q * 32) << 16) + static_cast<uint32_t>(acc * 256 * S + sub * 256);
+      };
       if (lo > 0) {
-        // stream-K contributor: park the int32 partial in this pair's slot
-        wait_local(&tfull[acc], (tl >> 1) & 1, 5);
+        // stream-K contributor: park the int32 partials in this pair's slot
+        wait_local(&tfull[acc], tpar, 5);
         tc_fence_after();
-        int32_t* slot = p.ws + (static_cast<size_t>(cid) * 2 + rank) * kSlot + static_cast<size_t>(mrow) * 16;
 #pragma unroll 1
-        for (int c0 = 0; c0 < TN; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(tbase + c0, r);
-          tmem_ld_wait();
-          int4* dst = reinterpret_cast<int4*>(slot + static_cast<size_t>(c0 / 16) * 2048);
+        for (int sub = 0; sub < S; ++sub) {
+          int32_t* slot = p.ws + (static_cast<size_t>(cid) * 2 + rank) * kSlot + sub * kSub;
+#pragma unroll 1
+          for (int c0 = cbeg; c0 < cend; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tbase_of(sub) + c0, r);
+            tmem_ld_wait();
 #pragma unroll
-          for (int v = 0; v < 4; ++v)
-            __stcg(dst + v, make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
-                                      static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3])));
+            for (int v = 0; v < 4; ++v)
+              __stcg(reinterpret_cast<int4*>(slot + part_off(c0 / 16, v, mrow)),
+                     make_int4(static_cast<int>(r[4 * v]), static_cast<int>(r[4 * v + 1]),
+                               static_cast<int>(r[4 * v + 2]), static_cast<int>(r[4 * v + 3])));
+          }
         }
         __threadfence();
         tc_fence_before();
-        named_bar(2, 128);
-        if (e == 0) st_release_gpu(p.counters + cid * 2 + rank, 1u);
+        named_bar(2, kEpiThreads);
+        if (et == 0) st_release_gpu(p.counters + cid * 2 + rank, 1u);
         __syncwarp();
         if (lane == 0) arrive_remote(tempty_leader + acc * 8);
         continue;
@@ -628,8 +804,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
         while (cid + 1 + npart < ncl && sk_begin(U, cid + 1 + npart, ncl) < tend) ++npart;
       }
       // per-tile scales (all four epilogue warps)
-      s_rs[e] = (p.rs && m0 + e < p.M) ? p.rs[m0 + e] : 0.0f;
-      for (int i = e; i < TN; i += 128) {
+      for (int i = et; i < S * 128; i += kEpiThreads) {
+        const int mm = m0_of(i >> 7) + (i & 127);
+        s_rs[i] = (p.rs && mm < p.M) ? p.rs[mm] : 0.0f;
+      }
+      for (int i = et; i < TN; i += kEpiThreads) {
         s_s1[i] = (p.s1 && n0 + i < p.N) ? p.s1[n0 + i] : 0.0f;
         s_bias[i] = (p.bias && n0 + i < p.N) ? p.bias[n0 + i] : 0.0f;
       }
@@ -639,71 +818,112 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
           while (ld_acquire_gpu(p.counters + (cid + c) * 2 + rank) == 0) watchdog(n, 9, 0);
         }
       }
-      named_bar(2, 128);
-      if (npart && e == 0)  // every thread has seen the flags: re-arm them for the next launch
+      named_bar(2, kEpiThreads);
+      if (npart && et == 0)  // every thread has seen the flags: re-arm them for the next launch
         for (int c = 1; c <= npart; ++c) p.counters[(cid + c) * 2 + rank] = 0u;
-      const int32_t* part =
-          npart ? p.ws + (static_cast<size_t>(cid + 1) * 2 + rank) * kSlot + static_cast<size_t>(mrow) * 16 : nullptr;
-      wait_local(&tfull[acc], (tl >> 1) & 1, 5);
+      wait_local(&tfull[acc], tpar, 5);
       tc_fence_after();
-      if (npart) {
-        // fold the contributors' partials into this thread's TMEM row (exact int32)
+      if (et == 0 && tl < 8) pf_stamp(p, 9, 2 * tl);
 #pragma unroll 1
-        for (int c0 = 0; c0 < TN; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(tbase + c0, r);
-          tmem_ld_wait();
-          add_partials16(r, part, npart, pstride, c0 / 16);
-          tmem_st16(tbase + c0, r);
+      for (int sub = 0; sub < S; ++sub) {
+        const uint32_t tbase = tbase_of(sub);
+        const int m0 = m0_of(sub);
+        // fold the contributors' partials into this thread's TMEM row (exact
+        // int32).  An owner segment is always its pair's LAST, so the Xq / B
+        // rings are idle: each contributor's 128-row partial (128 KB) comes in
+        // with one bulk copy instead of per-thread L2 round trips.
+#pragma unroll 1
+        for (int c = 1; c <= npart; ++c) {
+          const int32_t* part = p.ws + (static_cast<size_t>(cid + c) * 2 + rank) * kSlot + sub * kSub;
+          if (et == 0) {
+            mbar_arrive_expect_tx(fbar, static_cast<uint32_t>(kSub * 4));
+            bulk_load(sA, part, static_cast<uint32_t>(kSub * 4), fbar);
+          }
+          wait_local(fbar, fphase, 10);
+          fphase ^= 1u;
+          const int32_t* sp = reinterpret_cast<const int32_t*>(sA);
+#pragma unroll 1
+          for (int c0 = cbeg; c0 < cend; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16(tbase + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int4 x = *reinterpret_cast<const int4*>(sp + part_off(c0 / 16, v, mrow));
+              r[4 * v + 0] += static_cast<uint32_t>(x.x);
+              r[4 * v + 1] += static_cast<uint32_t>(x.y);
+              r[4 * v + 2] += static_cast<uint32_t>(x.z);
+              r[4 * v + 3] += static_cast<uint32_t>(x.w);
+            }
+            tmem_st16(tbase + c0, r);
+          }
+          tmem_st_wait();
+          named_bar(2, kEpiThreads);  // every row read before the next partial overwrites the buffer
         }
-        tmem_st_wait();
-      }
-      const float rsm = s_rs[mrow];
-      if (p.tma_out && !p.acc_out) {
-        const int mbox = m0 + q * 32;
+        const float rsm = s_rs[sub * 128 + mrow];
+        if (et == 0 && tl < 8) pf_stamp(p, 9, 512 + 4 * tl + sub);
+        if (m0 >= p.M) continue;  // a token quarter past M: nothing to store
+        if (S == 2 && p.out && p.vec_ok && !p.acc_out) {
+          if constexpr (S == 2) {
+            if (p.out_f16)
+              epi_direct<TN, true>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+            else
+              epi_direct<TN, false>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+          }
+        } else if (S == 1 && p.tma_out && !p.acc_out) {
+          if constexpr (S == 1) {
+            const int mbox = m0 + q * 32;
 #define DGQ_EPI2(F16_, MODE_, BIAS_) \
   epi_rows<TN, F16_, MODE_, BIAS_>(p, tbase, rsm, s_s1, s_bias, stg0, &tmY, n0, mbox)
-        const bool b = p.bias != nullptr, f = p.fp16_mode != 0;
-        if (p.out_f16) {
-          if (f) { if (b) DGQ_EPI2(true, true, true); else DGQ_EPI2(true, true, false); }
-          else   { if (b) DGQ_EPI2(true, false, true); else DGQ_EPI2(true, false, false); }
-        } else {
-          if (f) { if (b) DGQ_EPI2(false, true, true); else DGQ_EPI2(false, true, false); }
-          else   { if (b) DGQ_EPI2(false, false, true); else DGQ_EPI2(false, false, false); }
-        }
+            if (p.out_f16) {
+              if (f_) { if (b_) DGQ_EPI2(true, true, true); else DGQ_EPI2(true, true, false); }
+              else    { if (b_) DGQ_EPI2(true, false, true); else DGQ_EPI2(true, false, false); }
+            } else {
+              if (f_) { if (b_) DGQ_EPI2(false, true, true); else DGQ_EPI2(false, true, false); }
+              else    { if (b_) DGQ_EPI2(false, false, true); else DGQ_EPI2(false, false, false); }
+            }
 #undef DGQ_EPI2
-      } else {
-        const int m = m0 + mrow;
+          }
+        } else {
+          const int m = m0 + mrow;
 #pragma unroll 1
-        for (int c0 = 0; c0 < TN; c0 += 16) {
-          if (n0 + c0 >= p.N) break;
-          uint32_t r[16];
-          tmem_ld16(tbase + c0, r);
-          tmem_ld_wait();
-          if (m >= p.M) continue;
+          for (int c0 = cbeg; c0 < cend; c0 += 16) {
+            if (n0 + c0 >= p.N) break;
+            uint32_t r[16];
+            tmem_ld16(tbase + c0, r);
+            tmem_ld_wait();
+            if (m >= p.M) continue;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int n = n0 + c0 + k;
-            if (n >= p.N) break;
-            const int32_t a = static_cast<int32_t>(r[k]);
-            if (p.acc_out) p.acc_out[static_cast<size_t>(m) * p.ld_acc + n] = a;
-            if (p.out) {
-              float y = p.fp16_mode ? epilogue_f16mode(a, rsm, s_s1[c0 + k]) : epilogue_f32(a, rsm, s_s1[c0 + k]);
-              if (p.bias) y = __fadd_rn(y, s_bias[c0 + k]);
-              if (p.out_f16)
-                static_cast<__half*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = fp16_ref(y);
-              else
-                static_cast<float*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = y;
+            for (int k = 0; k < 16; ++k) {
+              const int n = n0 + c0 + k;
+              if (n >= p.N) break;
+              const int32_t a = static_cast<int32_t>(r[k]);
+              if (p.acc_out) p.acc_out[static_cast<size_t>(m) * p.ld_acc + n] = a;
+              if (p.out) {
+                float y = p.fp16_mode ? epilogue_f16mode(a, rsm, s_s1[c0 + k]) : epilogue_f32(a, rsm, s_s1[c0 + k]);
+                if (p.bias) y = __fadd_rn(y, s_bias[c0 + k]);
+                if (p.out_f16)
+                  static_cast<__half*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = fp16_ref(y);
+                else
+                  static_cast<float*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = y;
+              }
             }
           }
         }
       }
+      if (et == 0 && tl < 8) pf_stamp(p, 9, 512 + 4 * tl + 2);
       tc_fence_before();
       __syncwarp();
+      if (et == 0 && tl < 8) pf_stamp(p, 9, 2 * tl + 1);
       if (lane == 0) arrive_remote(tempty_leader + acc * 8);  // the leader's tempty[acc]
-      named_bar(2, 128);  // scales of the next tile are rewritten
+      named_bar(2, kEpiThreads);  // scales of the next tile are rewritten
     }
     if (lane == 0) bulk_wait_all();
+    if (p.dbg && e == 0 && blockIdx.x < 1024) {  // tools/pf_trace.py: epilogue done
+      uint64_t g;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+      p.dbg[8 * 1024 + blockIdx.x] = g;
+    }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   tc_fence_before();
@@ -718,54 +938,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::kThreads, 1)
 
 using namespace dgqk;
 
-size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride) {
-  return 1024 + pf::kSA * pf::kATile + pf::kSC * chunk_stride + pf::kSB * pf::kBTile + pf::kStaging +
-         (2 * pf::kSA + 2 * pf::kSC + 2 * pf::kSB + 4) * 8 + 16 + (128 + 256 + 256) * 4;
+template <int S>
+static size_t smem_bytes_s(uint32_t chunk_stride) {
+  using C = pf::Cfg<S>;
+  return 1024 + static_cast<size_t>(C::kSA) * S * pf::kATile + C::kSC * chunk_stride + C::kSB * pf::kBTile +
+         C::kEpiWarps * pf::kStagingPerWarp + (2 * C::kSA + 2 * C::kSC + 2 * C::kSB + 5) * 8 + 32 +
+         (128 * S + 256 + 256) * 4;
 }
 
-template <int TN>
+size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride, int sub) {
+  return sub == 2 ? smem_bytes_s<2>(chunk_stride) : smem_bytes_s<1>(chunk_stride);
+}
+
+template <int TN, int S>
 static int max_active_pairs() {
   // persistent + stream-K spin-waits need every pair co-resident: ask the
   // occupancy calculator how many 2-CTA clusters of this kernel fit at once
-  static int cached[2] = {0, 0};
-  int& c = cached[TN == 256 ? 0 : 1];
-  if (c) return c;
+  static int cached = 0;
+  if (cached) return cached;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int n = sms / 2;
-  const size_t smem = dgq_prefill2_smem_bytes(static_cast<uint32_t>(dgq_layout::chunk_bytes(128)));
-  auto kern = k_dgq_prefill2<TN>;
+  const size_t smem = smem_bytes_s<S>(static_cast<uint32_t>(dgq_layout::chunk_bytes(128)));
+  auto kern = k_dgq_prefill2<TN, S>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
       cudaSuccess) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * n);
-    cfg.blockDim = dim3(pf::kThreads);
+    cfg.blockDim = dim3(pf::Cfg<S>::kThreads);
     cfg.dynamicSmemBytes = smem;
     int q = 0;
     if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0 && q < n) n = q;
   }
   cudaGetLastError();
-  c = n;
-  return c;
+  cached = n;
+  return cached;
 }
 
-int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k) {
-  const int pairs = tn == 128 ? max_active_pairs<128>() : max_active_pairs<256>();
-  const long long tiles = static_cast<long long>((M + 255) / 256) * ((N + tn - 1) / tn);
+int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int sub) {
+  const int pairs = sub == 2 ? max_active_pairs<256, 2>()
+                             : (tn == 128 ? max_active_pairs<128, 1>() : max_active_pairs<256, 1>());
+  const long long tiles = static_cast<long long>((M + 256 * sub - 1) / (256 * sub)) * ((N + tn - 1) / tn);
   const long long work = stream_k ? tiles * k_blocks : tiles;
   return static_cast<int>(work < pairs ? work : pairs);
 }
 
-template <int TN>
+template <int TN, int S>
 static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
                              cudaStream_t st) {
-  const size_t smem = dgq_prefill2_smem_bytes(p.chunk_stride);
-  auto kern = k_dgq_prefill2<TN>;
+  const size_t smem = smem_bytes_s<S>(p.chunk_stride);
+  auto kern = k_dgq_prefill2<TN, S>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN, p.k_blocks, p.stream_k != 0));
-  cfg.blockDim = dim3(pf::kThreads);
+  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN, p.k_blocks, p.stream_k != 0, S));
+  cfg.blockDim = dim3(pf::Cfg<S>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -779,6 +1006,7 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
 }
 
 cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,
-                                bool pdl, cudaStream_t st) {
-  return tn == 128 ? launch_pf<128>(tmA, tmY, p, pdl, st) : launch_pf<256>(tmA, tmY, p, pdl, st);
+                                int sub, bool pdl, cudaStream_t st) {
+  if (sub == 2) return launch_pf<256, 2>(tmA, tmY, p, pdl, st);
+  return tn == 128 ? launch_pf<128, 1>(tmA, tmY, p, pdl, st) : launch_pf<256, 1>(tmA, tmY, p, pdl, st);
 }

@@ -311,15 +311,15 @@ def test_decode_kernel_matches_oracle(cuda, port, M, h, o, g):
 PREFILL_CASES = [
     # (M, h, o, g): persistent CTA-pair kernel (M >= 256): ragged M / N / K, odd tile counts, every group path
     (256, 512, 256, 128), (300, 1024, 384, 64), (513, 992, 1000, 32), (777, 2048, 640, 256), (1030, 384, 130, 128),
-
-
     # stream-K over many pairs: tiles split across 3+ pairs, owners with several contributors
     (1024, 2048, 1792, 128), (512, 7168, 768, 128),
 ]
 
 # debug mode bits (csrc/gemm.cu dgq_plan_gemm): 0x400 force K5p, 0x800 128-wide
 # pair tile, 0x2000 round-robin whole tiles instead of stream-K
-PAIR_MODES = {"sk256": 0x400, "sk128": 0x400 | 0x800, "rr256": 0x400 | 0x2000, "rr128": 0x400 | 0x800 | 0x2000}
+# 0x20000 one token sub-tile per CTA (256-token pair tiles; two from M >= 512 otherwise)
+PAIR_MODES = {"sk256": 0x400, "sk256s1": 0x400 | 0x20000, "sk128": 0x400 | 0x800, "rr256": 0x400 | 0x2000,
+              "rr128": 0x400 | 0x800 | 0x2000}
 
 
 @pytest.fixture(params=list(PAIR_MODES), ids=list(PAIR_MODES))
@@ -342,7 +342,7 @@ def test_prefill_pair_kernel_matches_oracle(cuda, port, pair_kernel, M, h, o, g)
     out, w, q, rs, mx = port.dgq_forward(X, L, bias)
     acc_ref, _ = port.int8_gemm(q, w)
     CL = dgq.CudaLayer(_to_dgq(L))
-    assert CL.plan(M)["token_tile"] == 256
+    assert CL.plan(M)["token_tile"] in (256, 512)
     codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
     db = torch.from_numpy(bias).cuda()
     y32, acc = CL.linear(codes, drs, bias=db, out_dtype=torch.float32, want_acc=True)
@@ -369,7 +369,7 @@ def test_prefill_full_size_work_splits_agree(cuda, port, M, h, o):
     codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
     accs = {}
     try:
-        for name, mode in (("sk", 1), ("rr", 1 | 0x2000), ("one_cta", 1 | 0x1000)):
+        for name, mode in (("sk", 1), ("sk_s1", 1 | 0x20000), ("rr", 1 | 0x2000), ("one_cta", 1 | 0x1000)):
             lib.dgq_debug_set_decode(mode)
             y, acc = CL.linear(codes, drs, out_dtype=torch.float16, want_acc=True)
             y2 = CL.linear(codes, drs, out_dtype=torch.float16)  # TMA-store epilogue path
@@ -378,6 +378,7 @@ def test_prefill_full_size_work_splits_agree(cuda, port, M, h, o):
     finally:
         lib.dgq_debug_set_decode(1)
     assert torch.equal(accs["sk"], accs["rr"])
+    assert torch.equal(accs["sk"], accs["sk_s1"])
     assert torch.equal(accs["sk"], accs["one_cta"])
     w = CL.dequant_s8().cpu().numpy().astype(np.int64)
     q = codes[:, :h].cpu().numpy().astype(np.int64)
