@@ -117,6 +117,9 @@ __device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t parity)
       : "memory");
   return ok != 0;
 }
+#ifndef DGQ_PF_BACKOFF
+#define DGQ_PF_BACKOFF 0
+#endif
 #ifndef DGQ_PF_WATCHDOG
 #define DGQ_PF_WATCHDOG 0
 #endif
@@ -157,7 +160,12 @@ __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity, int
 }
 __device__ __forceinline__ void wait_local(uint64_t* bar, uint32_t parity, int id) {
   long long n = 0;
-  while (!mbar_try_wait(bar, parity)) watchdog(n, id, parity);
+  while (!mbar_try_wait(bar, parity)) {
+#if DGQ_PF_BACKOFF
+    __nanosleep(DGQ_PF_BACKOFF);
+#endif
+    watchdog(n, id, parity);
+  }
 }
 // converged-warp issue (one lane elected inside the asm)
 __device__ __forceinline__ void mma2_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
