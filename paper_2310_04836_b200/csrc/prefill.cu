@@ -502,6 +502,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
   const bool leader = rank == 0;
   const int KB = p.k_blocks;
   const int n_tiles = (p.N + 127) / 128;  // 128-channel weight tiles (prepared chunks)
+  // tiles are token-tile major (t = mt * n_pairs + nt): the stream-K ranges of
+  // the pairs working on different token tiles sweep the same weight tiles at
+  // the same time, so each weight chunk comes from HBM once and is re-read from
+  // L2 (n-major order re-read every chunk per token tile: 3.7x the unique HBM
+  // bytes on OPT-30B fc1, profiles/ncu_summary_r01c.json)
   const int m_pairs = (p.M + 256 * S - 1) / (256 * S), n_pairs = (p.N + TN - 1) / TN;
   const int total = m_pairs * n_pairs;
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
@@ -581,7 +586,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
         const int t = c.t, kb = c.kb;
         si.advance(c);
         si.advance(c);
-        const int nt = t / m_pairs;
+        const int nt = t % n_pairs;
         // the prepared 128-channel weight tile this CTA dequantises (from)
         const int ctile = TN == 256 ? nt * 2 + static_cast<int>(rank) : nt;
         const bool has_w = ctile < n_tiles;
@@ -613,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
         si.advance(c);
         const int s = i % kSA;
         wait_local(&aempty[s], ((i / kSA) & 1) ^ 1, 7);
-        const int mpair = (t % m_pairs) * 256 * S;
+        const int mpair = (t / n_pairs) * 256 * S;
         // token quarters entirely past M are not loaded: their rows of D are never stored
         if (leader) {
           uint32_t tx = 0;
@@ -699,7 +704,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
       for (int it = grp; it < n; it += kDqGroups) {
         const int t = cu.t;
         for (int i = 0; i < kDqGroups; ++i) si.advance(cu);
-        const int nt = t / m_pairs;
+        const int nt = t % n_pairs;
         const bool has_w = (TN == 256 ? nt * 2 + static_cast<int>(rank) : nt) < n_tiles;
         const int s = it % kSC, b = it % kSB;
         wait_local(&cfull[s], (it / kSC) & 1, 4);
@@ -768,7 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
     uint32_t fphase = 0;
     int t, lo, hi;
     for (; si.next(t, lo, hi); ++tl) {
-      const int mt = t % m_pairs, nt = t / m_pairs;
+      const int mt = t / n_pairs, nt = t % n_pairs;
       const int acc = tl % kNAcc;
       const uint32_t tpar = (tl / kNAcc) & 1;
       const int n0 = nt * TN;

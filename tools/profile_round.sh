@@ -2,7 +2,7 @@
 # ncu evidence for a round (run under gpurun, one GPU): launch list of a short
 # bench run + one full capture per hot kernel.  Outputs in gpurun_out/.
 set -x
-T=${1:-r01}
+T=${1:-r01c}
 ncu --metrics gpu__time_duration.sum --clock-control none -c 160 --csv --log-file gpurun_out/launches_$T.csv \
     python bench.py --steps 2 --warmup 1 --no-detail --no-cpu > gpurun_out/bench_under_ncu_$T.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_dgq_prefill2 -s 1 -c 1 -o gpurun_out/${T}_prefill_fc1 -f \
