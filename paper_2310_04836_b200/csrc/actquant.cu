@@ -232,9 +232,8 @@ __global__ void __launch_bounds__(T) k_actquant_h_any(const __half* __restrict__
 // loads are skipped.
 template <bool kCheckX, bool kCheckK>
 __device__ __forceinline__ void smooth_chunk(const float (&x)[8], const float* __restrict__ kv,
-                                             const float* __restrict__ rkv, const uint8_t* __restrict__ kone, int c,
-                                             float (&q)[8]) {
-  if (kone && __ldg(kone + c)) {
+                                             const float* __restrict__ rkv, bool unit, int c, float (&q)[8]) {
+  if (unit) {
 #pragma unroll
     for (int t = 0; t < 8; ++t) q[t] = x[t];
     return;
@@ -247,6 +246,25 @@ __device__ __forceinline__ void smooth_chunk(const float (&x)[8], const float* _
   const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
   const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
   div_chunk<kCheckX, kCheckK>(x, kk, rr, q);
+}
+
+// Bit v: chunk threadIdx.x-based index cbase + v*T is a unit-k chunk.  Built
+// once per kernel with all V flag loads in flight together (a flag load per
+// chunk inside the row loop was a dependent L2 round trip: 34 % of K1's stall
+// samples, profiles/ncu_summary_r01c.json era capture).
+template <int T, int V>
+__device__ __forceinline__ uint32_t unit_mask(const uint8_t* __restrict__ kone, int cbase, int C8) {
+  if (!kone) return 0u;
+  uint8_t f[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int c = cbase + v * T;
+    f[v] = c < C8 ? __ldg(kone + c) : 0;
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) m |= (f[v] ? 1u : 0u) << v;
+  return m;
 }
 
 template <int T, int V, int CL, bool kF16, bool kCheckK>
@@ -263,6 +281,7 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
   if (row >= M) return;  // grid is exactly M*CL; keeps the cluster barrier uniform
   const int C8 = K >> 3;
   const int cbase = part * T * V + threadIdx.x;
+  const uint32_t umask = unit_mask<T, V>(kone, cbase, C8);
   uint4 raw[V][kF16 ? 1 : 2];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -301,7 +320,7 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 #pragma unroll
         for (int t = 0; t < 8; ++t) x[t] = f[t];
       }
-      smooth_chunk<!kF16, kCheckK>(x, kv, rkv, kone, c, xv[v]);
+      smooth_chunk<!kF16, kCheckK>(x, kv, rkv, (umask >> v) & 1u, c, xv[v]);
 #pragma unroll
       for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
     }
@@ -378,6 +397,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
     dgqk::fence_mbar_init();
   }
   __syncthreads();
+  const uint32_t umask = unit_mask<T, V>(kone, static_cast<int>(threadIdx.x), C8);
   int it = 0;
   if (threadIdx.x == 0) {
     if (static_cast<int>(blockIdx.x) < M) issue(blockIdx.x, 0);
@@ -410,7 +430,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
           x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
           x[4] = bb.x; x[5] = bb.y; x[6] = bb.z; x[7] = bb.w;
         }
-        smooth_chunk<!kF16, kCheckK>(x, kv, rkv, kone, c, xv[v]);
+        smooth_chunk<!kF16, kCheckK>(x, kv, rkv, (umask >> v) & 1u, c, xv[v]);
 #pragma unroll
         for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
       }
