@@ -49,6 +49,7 @@ print(f"median: issue->full {lat(1, 2):.3f}  full->bempty {lat(2, 3):.3f}  bempt
       f"done->mma {lat(4, 0):.3f}  issue->mma {lat(1, 0):.3f} us")
 ep = [(round(r(b[9][2 * i]), 2), round(r(b[9][2 * i + 1]), 2)) for i in range(8) if b[9][2 * i] > 0]
 print("CTA 0 epilogues (start, end) us:", ep)
+print("CTA 0 second-pass starts (dbg 8):", [[round(r(b[9][640 + 4 * i + j]), 2) for j in range(2)] for i in range(4) if b[9][640 + 4 * i] > 0])
 print("CTA 0 epilogue sub-tile starts / end:", [[round(r(b[9][512 + 4 * i + j]), 2) for j in range(3)] for i in range(4) if b[9][512 + 4 * i] > 0])
 st, en = b[7], b[8]
 ok = (st > 0) & (en > 0)
