@@ -172,6 +172,20 @@ dgq_status dgq_epilogue(const int32_t* dAcc, size_t lda, const float* dRowScale,
 dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K,
                                  size_t N, int64_t* max_abs_acc, void* stream);
 
+/* ---- calibration statistics --------------------------------
+ * The step before the path: from calibration activations dX [rows x h]
+ * (row-major f32, device) computes the smoothing vector and the static
+ * activation scale exactly as the reference's quantize_layer does
+ * (proj/src/pipeline.cpp:352-360): z = channel_maxima (proj/src/smoothing.cpp:9-24),
+ * k = compute_smooth(z, percentile) (proj/src/smoothing.cpp:26-49; with
+ * fp16_scales, k = max(1, fp16_round(k))), act_scale = static_act_scale of the
+ * smoothed rows (proj/src/pipeline.cpp:96-101; fp16_round'ed with fp16_scales).
+ * k_out [h], threshold_out and act_scale_out are HOST pointers; the call
+ * synchronises the stream.  DGQ_EINVAL for a percentile outside (0, 1) or a
+ * non-positive threshold (all-zero calibration), as the reference throws. */
+dgq_status dgq_calibrate(const float* dX, size_t rows, size_t h, size_t ldx, float percentile, int fp16_scales,
+                         float* k_out, float* threshold_out, float* act_scale_out, void* stream);
+
 /* ---- host-buffer API: the reference's calling convention --------------------
  * Host arrays in (reference layouts), host arrays out; each call uploads,
  * runs the CUDA kernels on a per-thread stream of the CURRENT device and

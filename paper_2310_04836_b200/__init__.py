@@ -8,14 +8,15 @@ and the column-parallel multi-GPU wrapper in `parallel`.
 """
 from ._lib import (DgqError, FormatError, InvalidArgument, OverflowRuntimeError,  # noqa: F401
                    ValidationError, lib)
-from .api import (ActQuant, CudaLayer, DgqLayer, ForwardResult, IntGemmResult, clip_interval,  # noqa: F401
+from .api import (ActQuant, CudaLayer, DgqLayer, ForwardResult, IntGemmResult, calibrate, clip_interval,  # noqa: F401
                   dequantize_to_f32, dequantize_to_s8, dgq_forward, epilogue, fp16_round, host_forward,
                   int8_gemm, layer_from_bytes, linear_multi, quantize_activations, segmented_gemm_reference,
                   validate_layer)
 from .synth import gen_synthetic, pack_u4, random_layer, unpack_u4  # noqa: F401
 
 __all__ = [
-    "ActQuant", "CudaLayer", "DgqLayer", "ForwardResult", "IntGemmResult", "clip_interval", "dequantize_to_f32",
+    "ActQuant", "CudaLayer", "DgqLayer", "ForwardResult", "IntGemmResult", "calibrate", "clip_interval",
+    "dequantize_to_f32",
     "dequantize_to_s8", "dgq_forward", "epilogue", "fp16_round", "int8_gemm", "layer_from_bytes",
     "quantize_activations", "validate_layer", "segmented_gemm_reference", "host_forward", "linear_multi", "gen_synthetic", "pack_u4", "random_layer", "unpack_u4",
     "DgqError", "FormatError", "InvalidArgument", "OverflowRuntimeError", "ValidationError", "lib",

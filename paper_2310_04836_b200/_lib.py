@@ -75,6 +75,7 @@ _SIGS = {
     "dgq_linear": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _i, _vp, _sz, _vp, _sz, _vp, _sz, _vp]),
     "dgq_forward_device": (_i, [_vp, _vp, _sz, _sz, _vp, _i, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
     "dgq_layer_dequant_s8": (_i, [_vp, _vp, _sz, _vp]),
+    "dgq_calibrate": (_i, [_vp, _sz, _sz, _sz, _f, _i, _vp, _vp, _vp, _vp]),
     "dgq_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp, _vp]),
     "dgq_int8_gemm": (_i, [_vp, _sz, _vp, _sz, _sz, _sz, _sz, _vp, _sz, C.POINTER(C.c_int64), _vp]),
     "dgq_epilogue": (_i, [_vp, _sz, _vp, _vp, _vp, _sz, _sz, _i, _i, _vp, _sz, _vp]),

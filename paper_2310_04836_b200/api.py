@@ -319,6 +319,24 @@ def _to_dev(a, dtype):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device=_dev(), dtype=dtype)
 
 
+def calibrate(X: torch.Tensor, percentile: float = 0.005, fp16_scales: bool = False):
+    """Calibration statistics on the GPU: the smoothing vector
+    and static activation scale the reference's quantize_layer derives from its
+    calibration rows (proj/src/pipeline.cpp:352-360) — k = compute_smooth(
+    channel_maxima(X), percentile) (proj/src/smoothing.cpp:9-49) and
+    act_scale = static_act_scale(X / k) (proj/src/pipeline.cpp:96-101).
+    X: cuda float32 [rows, h].  Returns (k float32 [h], act_scale, threshold)."""
+    import ctypes
+
+    assert X.is_cuda and X.dtype == torch.float32 and X.dim() == 2 and X.stride(1) == 1
+    k = np.empty(X.shape[1], np.float32)
+    thr, act = ctypes.c_float(0.0), ctypes.c_float(0.0)
+    check(lib().dgq_calibrate(_t_ptr(X), X.shape[0], X.shape[1], X.stride(0), float(percentile), int(fp16_scales),
+                              k.ctypes.data_as(ctypes.c_void_p), ctypes.cast(ctypes.pointer(thr), ctypes.c_void_p),
+                              ctypes.cast(ctypes.pointer(act), ctypes.c_void_p), _stream(X.device)))
+    return k, float(act.value), float(thr.value)
+
+
 def quantize_activations(X, layer: DgqLayer) -> ActQuant:
     """proj/src/kernel.cpp:14-44."""
     X = np.asarray(X) if not isinstance(X, torch.Tensor) else X

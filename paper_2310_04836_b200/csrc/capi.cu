@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -678,6 +679,57 @@ dgq_status dgq_forward_device(const dgq_layer* L, const float* dX, size_t M, siz
   if (s != DGQ_OK) return s;
   return dgq_linear(L, dXq, L->k_pad, dRs, M, dBias, out_dtype, 0, dY, ldy, nullptr, 0, dWorkspace, ws_bytes,
                     stream);
+}
+
+dgq_status dgq_calibrate(const float* dX, size_t rows, size_t h, size_t ldx, float percentile, int fp16_scales,
+                         float* k_out, float* threshold_out, float* act_scale_out, void* stream) {
+  if (!dX || !k_out) return fail(DGQ_EINVAL, "null argument");
+  if (rows == 0 || h == 0) return fail(DGQ_EINVAL, "empty calibration set");
+  if (ldx < h) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
+  if (rows > 0x7FFFFFFF || h > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too large");
+  if (!(percentile > 0.0f && percentile < 1.0f)) return fail(DGQ_EINVAL, "percentile must be in (0, 1)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* dz = nullptr;
+  float* dk = nullptr;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dz), (h + 1) * sizeof(unsigned), st));
+  DGQ_CUDA(cudaMemsetAsync(dz, 0, (h + 1) * sizeof(unsigned), st));
+  DGQ_CUDA(dgq_launch_colmax(dX, ldx, static_cast<int>(rows), static_cast<int>(h), dz, st));
+  std::vector<float> z(h);
+  DGQ_CUDA(cudaMemcpyAsync(z.data(), dz, h * sizeof(float), cudaMemcpyDeviceToHost, st));
+  DGQ_CUDA(cudaStreamSynchronize(st));
+  // compute_smooth (proj/src/smoothing.cpp:26-49): rank-th largest channel maximum
+  size_t rank = static_cast<size_t>(std::ceil(static_cast<double>(percentile) * static_cast<double>(h)));
+  rank = std::max<size_t>(rank, 1);
+  std::vector<float> sorted = z;
+  std::nth_element(sorted.begin(), sorted.begin() + (rank - 1), sorted.end(), std::greater<float>());
+  const float threshold = sorted[rank - 1];
+  if (!(threshold > 0.0f)) {
+    cudaFreeAsync(dz, st);
+    return fail(DGQ_EINVAL, "smoothing undefined: percentile threshold is not positive (all-zero calibration?)");
+  }
+  for (size_t j = 0; j < h; ++j) {
+    float v = std::max(1.0f, z[j] / threshold);
+    if (fp16_scales) v = std::max(1.0f, dgq_fp16_round(v));  // proj/src/pipeline.cpp:354-356
+    k_out[j] = v;
+  }
+  if (threshold_out) *threshold_out = threshold;
+  if (act_scale_out) {
+    DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dk), h * sizeof(float), st));
+    DGQ_CUDA(cudaMemcpyAsync(dk, k_out, h * sizeof(float), cudaMemcpyHostToDevice, st));
+    DGQ_CUDA(dgq_launch_smooth_absmax(dX, ldx, static_cast<int>(rows), static_cast<int>(h), dk, dz + h, st));
+    unsigned bits = 0;
+    DGQ_CUDA(cudaMemcpyAsync(&bits, dz + h, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    DGQ_CUDA(cudaStreamSynchronize(st));
+    float absmax;
+    std::memcpy(&absmax, &bits, sizeof(float));
+    // static_act_scale (proj/src/pipeline.cpp:96-101), kScaleFloor = 1e-8f
+    float s = static_cast<float>(std::max(static_cast<double>(absmax) / 127.0, static_cast<double>(1e-8f)));
+    if (fp16_scales) s = dgq_fp16_round(s);  // proj/src/pipeline.cpp:361
+    *act_scale_out = s;
+    cudaFreeAsync(dk, st);
+  }
+  cudaFreeAsync(dz, st);
+  return DGQ_OK;
 }
 
 dgq_status dgq_layer_dequant_s8(const dgq_layer* L, int8_t* dW, size_t ldw, void* stream) {

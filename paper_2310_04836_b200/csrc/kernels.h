@@ -181,3 +181,9 @@ cudaError_t dgq_launch_segmented(const int8_t* Xq, size_t ldx, const float* rs, 
                                  float* y, size_t ldy, cudaStream_t st);
 // dequantize_to_f32 (proj/src/format.cpp:143-154) from W_s8 [h x o].
 cudaError_t dgq_launch_dequant_f32(const int8_t* w, const float* s1, int h, int o, float* out, cudaStream_t st);
+
+// calibration statistics (calib.cu): z (uint bits of non-negative floats) must
+// be zero on entry; out likewise
+cudaError_t dgq_launch_colmax(const float* X, size_t ldx, int rows, int h, unsigned* z, cudaStream_t st);
+cudaError_t dgq_launch_smooth_absmax(const float* X, size_t ldx, int rows, int h, const float* k, unsigned* out,
+                                     cudaStream_t st);

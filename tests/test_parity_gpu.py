@@ -556,3 +556,29 @@ def test_actq_extreme_values_and_huge_k(cuda, port, M):
         codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
         assert np.array_equal(codes[:, :K].cpu().numpy(), q)
         assert np.array_equal(bits(drs.cpu().numpy()), bits(rs))
+
+
+@pytest.mark.parametrize("rows,h,pct,fp16", [(256, 7168, 0.005, False), (64, 1000, 0.01, True), (3, 33, 0.5, False),
+                                             (1024, 4096, 0.005, True)])
+def test_gpu_calibration_matches_reference(cuda, port, rows, h, pct, fp16):
+    # channel_maxima -> compute_smooth -> static_act_scale on the
+    # GPU equals the reference's (proj/src/smoothing.cpp:9-49, pipeline.cpp:96-101, :352-361)
+    X = port.gen_synthetic(rows, h, 31 + h, 3, 50.0, 7)
+    k_ref, thr_ref = port.smooth_from_calib(X, pct)
+    if fp16:
+        k_ref = np.maximum(np.float32(1.0), port.fp16_round_array(k_ref).astype(np.float32))
+    absmax = np.float32(np.abs(X / k_ref).max())
+    act_ref = np.float32(max(np.float64(absmax) / 127.0, np.float64(np.float32(1e-8))))
+    if fp16:
+        act_ref = np.float32(port.fp16_round(float(act_ref)))
+    k, act, thr = dgq.calibrate(torch.from_numpy(X).cuda(), pct, fp16)
+    assert np.array_equal(k.view(np.uint32), k_ref.astype(np.float32).view(np.uint32))
+    assert np.float32(thr) == np.float32(thr_ref)
+    assert np.float32(act).view(np.uint32) == act_ref.view(np.uint32)
+
+
+def test_gpu_calibration_errors(cuda):
+    with pytest.raises(dgq.InvalidArgument):
+        dgq.calibrate(torch.zeros(4, 64, device="cuda"))  # all-zero calibration: threshold not positive
+    with pytest.raises(dgq.InvalidArgument):
+        dgq.calibrate(torch.ones(4, 64, device="cuda"), percentile=1.0)
