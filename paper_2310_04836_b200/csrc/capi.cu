@@ -555,7 +555,7 @@ static dgq_status run_decode(const DecodeSub* subs, int count, int g, size_t k_p
   d.ld_acc = ld_acc;
   d.ws = static_cast<int32_t*>(ws);
   d.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + pl.ws_bytes);
-  d.dbg = (dgq_debug_decode_mode() >> 1) & 0x7F;
+  d.dbg = ((dgq_debug_decode_mode() >> 1) & 0x7F) | ((dgq_debug_decode_mode() >> 12) & 0x1C00) | ((dgq_debug_decode_mode() >> 7) & 0x380);  // tools: mode bits 14-16, 22-24 -> dbg bits 7-9, 10-12
   d.trace = g_dbg_ts;
   d.trace_cta = 0;
   DGQ_CUDA(dgq_launch_decode(pl.bn, tmB, d, pl.ctas, pl.pdl != 0, st));

@@ -210,7 +210,24 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (p.dbg & 1024) {
+    // tools/dec_gap.py: the weight stream alone (one producer lane, every other
+    // role idle) — separates the copy engine from the pipeline's cost at the
+    // kernel boundary
+    if (threadIdx.x == 0 && nu > 0) {
+      StageWalk w;
+      w.init(u0, nu, KB, ku);
+      for (; w.valid(); w.next(KB, ku)) {
+        const int sl = w.idx % SL;
+        if (w.idx >= SL) mbar_wait(&full[sl], ((w.idx / SL) - 1) & 1);
+        mbar_arrive_expect_tx(&full[sl], w.cnt * p.chunk_bytes);
+        bulk_load(sC + sl * stage_cb, dec::chunk_addr(p, w.tile, w.kb), w.cnt * p.chunk_bytes, &full[sl]);
+      }
+      for (int i = (w.idx > SL ? w.idx - SL : 0); i < w.idx; ++i) mbar_wait(&full[i % SL], (i / SL) & 1);
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
+    if ((p.dbg & 2048) && threadIdx.x == 32) asm volatile("griddepcontrol.wait;" ::: "memory");  // tools
+  } else if (warp == 0) {
     // ------------------------------ producer ------------------------------
     // one bulk copy of the stage's contiguous chunks + one 3-D TMA box of its
     // Xq tiles (large requests keep the per-CTA TMA queue streaming)
@@ -264,7 +281,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
         mbar_wait(&afull[sa], (i / kSA) & 1);
         mbar_wait(&dempty[sd], ((i >> sdl) & 1) ^ 1);
         tc_fence_after();
-        for (int c = mw; c < w.cnt; c += kMmaWarps) {
+        for (int c = mw; c < w.cnt && !(p.dbg & 1); c += kMmaWarps) {  // tools: bit 0 skips the MMAs
           const uint64_t db = umma_desc_sw128(smem_u32(sB + (s * UPS + c) * kBBytes));
           const uint32_t a0 = tm + (sa * UPS + c) * 32;
           const uint32_t d0 = tm + kDCol0 + sd * dslot + c * unit_dcols;
@@ -272,9 +289,17 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
           for (int kk = 0; kk < 4; ++kk)  // K = 32 per MMA: +8 TMEM columns of A, +32 B of the B row
             mma_i8_ts_warp(d0 + qoff[kk], a0 + kk * 8, db + 2 * kk, kIdesc, acc_in[kk]);
         }
-        mma_commit_warp(&empty[s]);
-        mma_commit_warp(&aempty[sa]);
-        mma_commit_warp(&dfull[sd]);
+        if (p.dbg & 1) {  // tools: no tcgen05 at all -> plain arrives
+          if (lane == 0) {
+            mbar_arrive(&empty[s]);
+            mbar_arrive(&aempty[sa]);
+            mbar_arrive(&dfull[sd]);
+          }
+        } else {
+          mma_commit_warp(&empty[s]);
+          mma_commit_warp(&aempty[sa]);
+          mma_commit_warp(&dfull[sd]);
+        }
         if (mw == 0 && lane == 0) dec::trace_stamp(p, 1, i);
       }
     }
@@ -323,7 +348,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
             a[2 * k] = (((wv[k] & 0x0F0F0F0Fu) | 0x80808080u) - z) ^ 0x80808080u;
             a[2 * k + 1] = ((((wv[k] >> 4) & 0x0F0F0F0Fu) | 0x80808080u) - z) ^ 0x80808080u;
           }
-          tmem_st16(tmem + taddr_lane + (sa * UPS + c) * 32 + half * 16, a);
+          if (!(p.dbg & 2)) tmem_st16(tmem + taddr_lane + (sa * UPS + c) * 32 + half * 16, a);
         }
       }
       tmem_st_wait();
@@ -370,8 +395,13 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
       for (int j0 = 0; j0 < UPS * 4 * BN && j0 < 128; j0 += 32) {
         if (j0 < ncols) {
           uint32_t d[32];
-          tmem_ld32(dcol + j0, d);
-          tmem_ld_wait();
+          if (p.dbg & 4) {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) d[jj] = 0;
+          } else {
+            tmem_ld32(dcol + j0, d);
+            tmem_ld_wait();
+          }
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
             const int j = j0 + jj;
@@ -390,7 +420,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
         const int t = w.tile;
         const long long tb = static_cast<long long>(t) * KB, te = tb + KB;
         if (seg_from_tile_start && w.kb + w.cnt == KB) {
-          dec::store_final<BN>(p, t, e, acc);
+          if (!(p.dbg & 4096)) dec::store_final<BN>(p, t, e, acc);
         } else {
           int32_t* ws = p.ws + static_cast<size_t>(t) * BN * 128 + e;
 #pragma unroll
@@ -413,7 +443,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
                 ws[m * 128] = 0;
               }
             }
-            dec::store_final<BN>(p, t, e, acc);
+            if (!(p.dbg & 4096)) dec::store_final<BN>(p, t, e, acc);
             if (e == 0) p.counters[t] = 0u;
           }
           named_bar(2, 128);  // s_flag is rewritten by the next segment

@@ -44,6 +44,15 @@ __global__ void __launch_bounds__(512, 1) k(const __grid_constant__ CUtensorMap 
       asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
                    : "=r"(ok) : "r"(su(&bar)), "r"((mode & 2) ? 1 : 0) : "memory");
   }
+  if ((mode & 32) && threadIdx.x == 0) {  // one 16 KB 1-D bulk copy, waited
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&bar)), "r"(16384));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::"r"(
+                     su(sm)), "l"(src + (blockIdx.x % 8) * 16384), "r"(su(&bar)) : "memory");
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0,1,0,p;}"
+                   : "=r"(ok) : "r"(su(&bar)) : "memory");
+  }
   uint64_t t0; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   uint64_t t = t0;
   while (t - t0 < (uint64_t)ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -62,7 +71,7 @@ int main() {
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int mode : {0, 1, 9, 16, 17, 25}) {
+  for (int mode : {0, 16, 32, 0, 16, 32}) {
     cudaGraph_t g; cudaGraphExec_t ge;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
     const int n = 20;
