@@ -236,11 +236,11 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
         const int sl = w.idx % SL;
         if (weights) {
           mbar_wait(&empty[sl], ((w.idx / SL) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[sl], w.cnt * p.chunk_bytes + ku * kBBytes);
+          mbar_arrive_expect_tx(&full[sl], w.cnt * p.chunk_bytes + ((p.dbg & 8) ? 0u : ku * kBBytes));
           bulk_load(sC + sl * stage_cb, dec::chunk_addr(p, w.tile, w.kb), w.cnt * p.chunk_bytes, &full[sl]);
           dec::trace_stamp(p, 0, w.idx);
         }
-        if (btile) tma_load_3d(sB + sl * UPS * kBBytes, &tmB, &full[sl], 0, 0, w.kb);
+        if (btile && !(p.dbg & 8)) tma_load_3d(sB + sl * UPS * kBBytes, &tmB, &full[sl], 0, 0, w.kb);  // tools: bit 3
       };
       // the first stage's weights do not depend on the previous kernel (PDL);
       // its Xq tiles do.  Each bulk request occupies the TMA engine for

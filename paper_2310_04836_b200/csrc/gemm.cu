@@ -581,7 +581,13 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
   const uint32_t cb = static_cast<uint32_t>(dgq_layout::chunk_bytes(g > 0 ? g : 128));
   const long long t256_ = static_cast<long long>((M + 255) / 256) * ((N + 255) / 256);
   const bool pair_ok = (g_decode_mode & 0x400) != 0 || sk || t256_ >= 6LL * (sm_count() / 2);
-  if (fused && M >= 256 && pair_ok && (g_decode_mode & 0x1000) == 0 && !force_bn && !force_splits &&
+  // K5p from 256 tokens; between 64 and 256 only for large weight matrices,
+  // whose stream-K pairs outrun the one-CTA kernel (tools/decode_sweep.py:
+  // OPT-30B fc2 at M = 128 / 192: 56 vs 93 / 142 us) while small ones keep
+  // the one-CTA kernel (K5p has a ~30 us floor: 4096^2 at M = 64 takes 29 vs 12 us)
+  const bool big_w = static_cast<double>(N) * K_pad >= 100e6;
+  const int pair_min_m = (g_decode_mode & 0x400) ? 33 : (big_w ? 64 : 256);  // tools: 0x400 admits 33 <= M
+  if (fused && M >= pair_min_m && pair_ok && (g_decode_mode & 0x1000) == 0 && !force_bn && !force_splits &&
       dgq_prefill2_smem_bytes(cb, 1) <= 232448) {
     const int pairs = sm_count() / 2;
     const long long mp = (M + 255) / 256;
@@ -595,8 +601,14 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
     pl.pair_tn = ((g_decode_mode & 0x800) != 0 || (!sk && c128 * 1.6 < c256)) ? 128 : 256;
     // two token sub-tiles per CTA (512-token pair tiles) from 512 tokens, with
     // stream-K balancing the tiles; mode bit 17 keeps one (256-token tiles)
-    pl.pair_sub = (sk && pl.pair_tn == 256 && M >= 512 && (g_decode_mode & 0x20000) == 0 &&
-                   dgq_prefill2_smem_bytes(cb, 2) <= 232448) ? 2 : 1;
+    // two sub-tiles pay an exposed epilogue per segment for a ~30 % faster
+    // main loop: worth it from ~100 k-blocks of 512-token tiles per pair
+    // (tools/decode_sweep.py: OPT-30B fc1 / fc2 at M >= 1024 and fc2 at 512
+    // gain 8-16 %, q at 2048 and 4096^2 shapes lose)
+    const long long t512 = ((M + 511) / 512) * static_cast<long long>((N + 255) / 256);
+    const bool s2_pays = t512 * kblocks >= 100LL * pairs;
+    pl.pair_sub = (sk && pl.pair_tn == 256 && M >= 512 && (s2_pays || (g_decode_mode & 0x40000000)) &&
+                   (g_decode_mode & 0x20000) == 0 && dgq_prefill2_smem_bytes(cb, 2) <= 232448) ? 2 : 1;
     pl.bn = 256 * pl.pair_sub;
     pl.nt = pl.pair_tn / 128;
     pl.m_tiles = static_cast<int>((M + pl.bn - 1) / pl.bn);

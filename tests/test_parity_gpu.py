@@ -313,12 +313,16 @@ PREFILL_CASES = [
     (256, 512, 256, 128), (300, 1024, 384, 64), (513, 992, 1000, 32), (777, 2048, 640, 256), (1030, 384, 130, 128),
     # stream-K over many pairs: tiles split across 3+ pairs, owners with several contributors
     (1024, 2048, 1792, 128), (512, 7168, 768, 128),
+    # mid M (the planner sends large weight matrices to K5p from 64 tokens)
+    (64, 1024, 512, 128), (200, 768, 384, 64),
 ]
 
 # debug mode bits (csrc/gemm.cu dgq_plan_gemm): 0x400 force K5p, 0x800 128-wide
 # pair tile, 0x2000 round-robin whole tiles instead of stream-K
-# 0x20000 one token sub-tile per CTA (256-token pair tiles; two from M >= 512 otherwise)
-PAIR_MODES = {"sk256": 0x400, "sk256s1": 0x400 | 0x20000, "sk128": 0x400 | 0x800, "rr256": 0x400 | 0x2000,
+# 0x20000 one token sub-tile per CTA (256-token pair tiles), 0x40000000 two from M >= 512
+# (otherwise the planner picks by work per pair)
+PAIR_MODES = {"sk256": 0x400, "sk256s1": 0x400 | 0x20000, "sk256s2": 0x400 | 0x40000000, "sk128": 0x400 | 0x800,
+              "rr256": 0x400 | 0x2000,
               "rr128": 0x400 | 0x800 | 0x2000}
 
 
@@ -369,7 +373,8 @@ def test_prefill_full_size_work_splits_agree(cuda, port, M, h, o):
     codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
     accs = {}
     try:
-        for name, mode in (("sk", 1), ("sk_s1", 1 | 0x20000), ("rr", 1 | 0x2000), ("one_cta", 1 | 0x1000)):
+        for name, mode in (("sk", 1), ("sk_s1", 1 | 0x20000), ("sk_s2", 1 | 0x40000000), ("rr", 1 | 0x2000),
+                           ("one_cta", 1 | 0x1000)):
             lib.dgq_debug_set_decode(mode)
             y, acc = CL.linear(codes, drs, out_dtype=torch.float16, want_acc=True)
             y2 = CL.linear(codes, drs, out_dtype=torch.float16)  # TMA-store epilogue path
@@ -379,6 +384,7 @@ def test_prefill_full_size_work_splits_agree(cuda, port, M, h, o):
         lib.dgq_debug_set_decode(1)
     assert torch.equal(accs["sk"], accs["rr"])
     assert torch.equal(accs["sk"], accs["sk_s1"])
+    assert torch.equal(accs["sk"], accs["sk_s2"])
     assert torch.equal(accs["sk"], accs["one_cta"])
     w = CL.dequant_s8().cpu().numpy().astype(np.int64)
     q = codes[:, :h].cpu().numpy().astype(np.int64)

@@ -12,10 +12,15 @@ import paper_2310_04836_b200 as dgq  # noqa: E402
 import ctypes  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
-if "--pair" in sys.argv:  # route M >= 256 to the CTA-pair prefill kernel (K5p)
+_mode = 1
+if "--pair" in sys.argv:  # route M >= 33 to the CTA-pair prefill kernel (K5p)
+    _mode |= 0x400
+if "--s1" in sys.argv:  # K5p with one token sub-tile per CTA (256-token pair tiles)
+    _mode |= 0x20000
+if _mode != 1:
     _l = dgq.lib()
     _l.dgq_debug_set_decode.argtypes = [ctypes.c_int]
-    _l.dgq_debug_set_decode(1 | 0x400)
+    _l.dgq_debug_set_decode(_mode)
 Ms = [int(v) for v in args] or [1, 16, 64, 512, 2048]
 shapes = [("q 7168x7168", 7168, 7168), ("fc1 7168x28672", 7168, 28672), ("fc2 28672x7168", 28672, 7168),
           ("llama7b up 4096x11008", 4096, 11008), ("c1 4096x4096", 4096, 4096)]
