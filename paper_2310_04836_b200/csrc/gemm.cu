@@ -565,6 +565,11 @@ int sm_count() {
 }  // namespace
 
 extern "C" void dgq_debug_set_decode(int mode) { g_decode_mode = mode; }
+namespace {
+int g_pair_cap = 0;
+}
+extern "C" void dgq_debug_set_pair_cap(int cap) { g_pair_cap = cap; }
+int dgq_prefill2_cluster_cap() { return g_pair_cap; }
 extern "C" int dgq_debug_decode_mode() { return g_decode_mode; }
 
 DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_bn, int force_splits) {

@@ -130,6 +130,7 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
 // sub = token sub-tiles per CTA (1: 256-token pair tiles, 2: 512-token pair tiles)
 size_t dgq_prefill2_smem_bytes(uint32_t chunk_stride, int sub);
 int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int sub);
+int dgq_prefill2_cluster_cap();  // tools: debug cap on K5p pairs (0 = none)
 // stream-K workspace: per pair two CTA partials of up to 2 x 128 x 256 int32, + flags
 constexpr size_t kPrefill2SlotBytes = 2 * 2 * 128 * 256 * 4;
 cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,

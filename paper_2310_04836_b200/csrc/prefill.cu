@@ -993,7 +993,22 @@ int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int
                              : (tn == 128 ? max_active_pairs<128, 1>() : max_active_pairs<256, 1>());
   const long long tiles = static_cast<long long>((M + 256 * sub - 1) / (256 * sub)) * ((N + tn - 1) / tn);
   const long long work = stream_k ? tiles * k_blocks : tiles;
-  return static_cast<int>(work < pairs ? work : pairs);
+  int n = static_cast<int>(work < pairs ? work : pairs);
+  if (stream_k && tiles > 0) {
+    // Whole tiles per pair when that is cheaper than splitting them: a split
+    // tile costs its owner a wait + fix-up and its contributors a partial
+    // store (~6 us per piece, tools/decode_sweep.py --cap: 4096^2 at M = 1024
+    // runs 64 whole tiles in 23 us on 64 pairs vs 31 us stream-K on 74).
+    const double t_kb = sub == 2 ? 0.70 : 0.49;  // us per k-block of one pair tile (measured)
+    const long long w = (tiles + pairs - 1) / pairs;
+    const double dp = static_cast<double>(w) * k_blocks * t_kb;
+    const long long pieces = tiles >= pairs ? 1 : (pairs + tiles - 1) / tiles;
+    const double skt = static_cast<double>(tiles) * k_blocks / pairs * t_kb + 6.0 * static_cast<double>(pieces);
+    if (dp <= skt) n = static_cast<int>((tiles + w - 1) / w);
+  }
+  const int cap = dgq_prefill2_cluster_cap();  // tools: planner experiments
+  if (cap > 0 && n > cap) n = cap;
+  return n;
 }
 
 template <int TN, int S>
