@@ -632,7 +632,16 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
   const int dec_bn = M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : 64));
   const int dec_gpk = g >= 128 ? 1 : (g > 0 ? 128 / g : 1);
   // K5d wins up to 32 tokens; at 33..64 the weight-tile-per-CTA kernel below is faster
-  if (fused && g >= 32 && g % 32 == 0 && M <= 32 && dec_bn * dec_gpk <= 128 && g_decode_mode && !force_bn &&
+  // K5d streams the weights with every SM from its first cycle but pays a
+  // fixed ~8 us; the one-CTA kernel is cheaper for small matrices and, as M
+  // grows, for medium ones (tools/decode_sweep.py --nodec: 4096^2 7.6 vs 8.6 us
+  // at M = 1, LLaMA-7B up 16.0 vs 16.8 at M = 16, OPT-30B q 19.7 vs 21.3 at
+  // M = 32; fc1 / fc2 always K5d)
+  const double kn = static_cast<double>(K_pad) * N;
+  const int dec_max_m = (g_decode_mode & 0x10000000) ? 64  // tools: mode bit 28 admits M <= 64
+                        : (g_decode_mode & 0x8000000) ? 32   // tools: mode bit 27: K5d up to 32 whatever the size
+                        : kn >= 100e6 ? 32 : kn >= 48e6 ? 16 : kn >= 32e6 ? 8 : 0;
+  if (fused && g >= 32 && g % 32 == 0 && M <= dec_max_m && dec_bn * dec_gpk <= 128 && g_decode_mode && !force_bn &&
       !force_splits) {
     // K5d: weight-streaming decode kernel, one persistent CTA per SM (stream-K)
     pl.decode = 1;

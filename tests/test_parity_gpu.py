@@ -264,8 +264,22 @@ def test_fp16_mode_epilogue_in_fused_kernel(cuda, port):
     assert np.array_equal(bits(y.cpu().numpy()), bits(ref))
 
 
+@pytest.fixture
+def decode_kernel():
+    """The planner keeps small matrices off K5d (the one-CTA kernel is faster
+    there); mode bit 27 sends every M <= 32 fused call to K5d so these small
+    parity shapes exercise it."""
+    import ctypes
+
+    lib = dgq.lib()
+    lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    lib.dgq_debug_set_decode(1 | 0x8000000)
+    yield
+    lib.dgq_debug_set_decode(1)
+
+
 @pytest.mark.parametrize("M", [1, 4, 16, 32])
-def test_decode_stream_k_is_exact_and_repeatable(cuda, port, M):
+def test_decode_stream_k_is_exact_and_repeatable(cuda, port, decode_kernel, M):
     # decode shapes (M <= 64) run K5d: persistent CTAs split the (tile, k-block)
     # units evenly, partial tiles are reduced exactly through the int32 workspace;
     # run three times to check the workspace and tile counters are left zeroed
@@ -289,7 +303,7 @@ DECODE_CASES = [
 
 
 @pytest.mark.parametrize("M,h,o,g", DECODE_CASES)
-def test_decode_kernel_matches_oracle(cuda, port, M, h, o, g):
+def test_decode_kernel_matches_oracle(cuda, port, decode_kernel, M, h, o, g):
     L = oracle.random_layer(h, o, g, seed=M + h + o + g)
     X = port.gen_synthetic(M, h, 5 + M, 3, 50.0, 3)
     bias = np.random.default_rng(M).uniform(-0.5, 0.5, o).astype(np.float32)
@@ -393,7 +407,7 @@ def test_prefill_full_size_work_splits_agree(cuda, port, M, h, o):
 
 
 @pytest.mark.parametrize("M", [1, 13, 32, 40])
-def test_linear_multi_shared_input(cuda, port, M):
+def test_linear_multi_shared_input(cuda, port, decode_kernel, M):
     # q / k / v style: three layers over one input, one K5d launch for M <= 32
     # (per-layer launches above); must equal the three separate linears bit for bit
     h, g = 1024, 128
@@ -422,6 +436,7 @@ def test_decode_and_prefill_orientations_agree(cuda, port):
     codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
     lib = dgq.lib()
     lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    lib.dgq_debug_set_decode(1 | 0x8000000)  # K5d (the planner would keep this small layer on the one-CTA kernel)
     a = CL.linear(codes, drs, out_dtype=torch.float32).cpu().numpy()
     lib.dgq_debug_set_decode(0)
     try:

@@ -15,6 +15,8 @@ args = [a for a in sys.argv[1:] if not a.startswith("--")]
 _mode = 1
 if "--pair" in sys.argv:  # route M >= 33 to the CTA-pair prefill kernel (K5p)
     _mode |= 0x400
+if "--dec64" in sys.argv:  # K5d (decode kernel) up to 64 tokens
+    _mode |= 0x10000000
 if "--s1" in sys.argv:  # K5p with one token sub-tile per CTA (256-token pair tiles)
     _mode |= 0x20000
 _cap = [int(a.split("=")[1]) for a in sys.argv[1:] if a.startswith("--cap=")]
@@ -22,6 +24,8 @@ if _cap:  # cap the K5p pair count (planner experiments)
     _l = dgq.lib()
     _l.dgq_debug_set_pair_cap.argtypes = [ctypes.c_int]
     _l.dgq_debug_set_pair_cap(_cap[0])
+if "--nodec" in sys.argv:  # never the decode kernel (one-CTA kernel below 256 tokens)
+    _mode &= ~1
 if _mode != 1:
     _l = dgq.lib()
     _l.dgq_debug_set_decode.argtypes = [ctypes.c_int]
