@@ -376,6 +376,44 @@ def decode_k5_bandwidth(layer, M, flush, reps=8):
     return out
 
 
+def decode_k5_streaming(layer, M, device, world, group):
+    """Steady-state algorithmic HBM GB/s of each distinct K5 shape at M tokens:
+    one CUDA graph of back-to-back launches over R copies of the layer whose
+    weights together exceed 2.2x L2 (every launch streams from HBM, as in a
+    decoder stack), time / R.  Complements decode_k5_bandwidth (one launch
+    after an L2 flush, which also carries the graph-launch latency)."""
+    import torch
+
+    from paper_2310_04836_b200.parallel import ColumnParallelLinear
+
+    out = {}
+    l2 = 126e6
+    for name, K, N in (("q", 7168, 7168), ("fc1", 7168, 28672), ("fc2", 28672, 7168)):
+        lin0 = layer.lin[name]
+        wb = K * lin0.shard / 2 + (K / GROUP) * lin0.shard * 1.5
+        copies = max(2, int(2.2 * l2 / wb) + 1)
+        L = tiled_layer(K, N, seed=500)
+        lins = [ColumnParallelLinear(L, int(os.environ.get("RANK", "0")), world, device, group)
+                for _ in range(copies)]
+        key = "q" if name in ("q", "k", "v") else name
+        codes, rs = layer.codes[key][:M], layer.rs[key][:M]
+        y = layer.y[name][:M]
+        g = _graph_of(lambda: [ln.linear(codes, rs, out=y) for ln in lins])
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        t = a.elapsed_time(b) * 1e-3 / copies
+        byts = M * K + 4 * M + wb + 4 * lin0.shard + 2 * M * lin0.shard
+        out[name] = {"us": t * 1e6, "GBps": byts / t / 1e9, "copies": copies}
+        del lins, g
+        torch.cuda.empty_cache()
+    return out
+
+
 def measure_int8_peak(device):
     """Dense INT8 tensor throughput of this GPU: cuBLASLt (torch._int_mm), the
     best of 10 CUDA-event timings after warm-up on three shapes (8192^3, the
@@ -571,6 +609,12 @@ def run_ours(args):
                 kb = decode_k5_bandwidth(layer, M, flush)
                 detail[f"decode_m{M}_k5_GBps"] = kb
                 detail[f"decode_m{M}_k5_hbm_frac"] = {n: v / hbm_peak for n, v in kb.items()}
+                try:
+                    st = decode_k5_streaming(layer, M, device, world, group)
+                    detail[f"decode_m{M}_k5_streaming"] = {n: dict(v, hbm_frac=v["GBps"] / hbm_peak)
+                                                          for n, v in st.items()}
+                except Exception as e:  # noqa: BLE001
+                    detail[f"decode_m{M}_k5_streaming"] = {"error": f"{type(e).__name__}: {e}"}
         detail["k5_tops_by_linear"] = {n: o / t / 1e12 for n, (t, o) in by_name.items()}
         detail["k1_GBps"] = k1_b / k1_t / 1e9
         detail["k1_GBps_by_input"] = {n: x / t / 1e9 for n, (t, x) in k1_by.items()}
