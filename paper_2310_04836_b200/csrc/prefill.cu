@@ -324,7 +324,7 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
     for (int c16 = 0; c16 < kCB; c16 += 16) {
       uint32_t (&cur)[16] = r[(c16 / 16) & 1];
       if (c16 + 16 < kCB) tmem_ld16(tbase + c0 + c16 + 16, r[((c16 / 16) + 1) & 1]);
-      if (!(p.dbg_flags & 2)) {
+      {
 #pragma unroll
         for (int c8 = 0; c8 < 16; c8 += 8) {
           const int c1 = c16 + c8;
@@ -332,17 +332,10 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
           const float4 sa = *reinterpret_cast<const float4*>(s_s1 + c0 + c1);
           const float4 sb = *reinterpret_cast<const float4*>(s_s1 + c0 + c1 + 4);
           const float sv[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
-          bool small = true;
+          // branch-free: a vote + branch per 8 values cost more than the
+          // conversion it avoided (tools/epi_probe.cu)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            bool ok;
-            y[k] = i2f_small(static_cast<int32_t>(cur[c8 + k]), ok);
-            small &= ok;
-          }
-          if (!__all_sync(0xffffffffu, small)) {  // some |acc| >= 2^22: the exact conversion
-#pragma unroll
-            for (int k = 0; k < 8; ++k) y[k] = __int2float_rn(static_cast<int32_t>(cur[c8 + k]));
-          }
+          for (int k = 0; k < 8; ++k) y[k] = __int2float_rn(static_cast<int32_t>(cur[c8 + k]));
 #pragma unroll
           for (int k = 0; k < 8; ++k) y[k] = __fmul_rn(__fmul_rn(y[k], rsm), sv[k]);
           if (kF16Mode) {
@@ -358,31 +351,19 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
           }
           if (kF16) {
             uint32_t h[4];
-            uint32_t tiny = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const __half2 hh = __floats2half2_rn(y[2 * k], y[2 * k + 1]);
-              h[k] = *reinterpret_cast<const uint32_t*>(&hh);
-              // IEEE rounding differs from fp16_round (proj/src/quant.cpp:33-35,
-              // |x| < 2^-24 -> signed zero) only where it produced +-2^-24 (0x0001)
-              tiny |= static_cast<uint32_t>((h[k] & 0x7FFFu) == 1u) |
-                      static_cast<uint32_t>((h[k] & 0x7FFF0000u) == 0x10000u);
+              uint32_t u = *reinterpret_cast<const uint32_t*>(&hh);
+              // fp16_round (proj/src/quant.cpp:33-35) flushes |x| < 2^-24 to a signed
+              // zero; selects, not a branch (tools/epi_probe.cu: the branch cost 2x)
+              const uint32_t lo = (__float_as_uint(y[2 * k]) >> 16) & 0x8000u;
+              const uint32_t hi = __float_as_uint(y[2 * k + 1]) & 0x80000000u;
+              u = fabsf(y[2 * k]) < 0x1p-24f ? ((u & 0xFFFF0000u) | lo) : u;
+              u = fabsf(y[2 * k + 1]) < 0x1p-24f ? ((u & 0x0000FFFFu) | hi) : u;
+              h[k] = u;
             }
-            if (tiny) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                uint32_t u = h[k];
-                if (fabsf(y[2 * k]) < 0x1p-24f) u = (u & 0xFFFF0000u) | ((__float_as_uint(y[2 * k]) >> 16) & 0x8000u);
-                if (fabsf(y[2 * k + 1]) < 0x1p-24f)
-                  u = (u & 0x0000FFFFu) | (__float_as_uint(y[2 * k + 1]) & 0x80000000u);
-                h[k] = u;
-              }
-            }
-            if (p.dbg_flags & 4) {  // tools: math only (no staging)
-              if ((h[0] ^ h[1] ^ h[2] ^ h[3]) == 0x12345678u) *static_cast<uint32_t*>(p.out) = h[0];
-            } else {
-              *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
-            }
+            *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
           } else {
             *reinterpret_cast<float4*>(myrow + (((c1 / 4) ^ sw) << 4)) = make_float4(y[0], y[1], y[2], y[3]);
             *reinterpret_cast<float4*>(myrow + (((c1 / 4 + 1) ^ sw) << 4)) = make_float4(y[4], y[5], y[6], y[7]);
@@ -391,28 +372,39 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
       }
       if (c16 + 16 < kCB) tmem_ld_wait();
     }
-    if (p.dbg_flags & 6) continue;
     __syncwarp();
     // 8 passes x (4 rows x 8 lanes x 16 bytes)
     const int ch = static_cast<int>(lane & 7);                 // 16-byte chunk of the row segment
     const int n = nbase + c0 + ch * (kF16 ? 8 : 4);            // first output column of the chunk
     constexpr int kPer = kF16 ? 8 : 4;                         // outputs per chunk
+    uint8_t* const out0 = static_cast<uint8_t*>(p.out) + (static_cast<size_t>(mrow0) * p.ldy + n) * (kF16 ? 2 : 4);
+    const size_t row_bytes = p.ldy * (kF16 ? 2 : 4);
+    if (mrow0 + 32 <= p.M && nbase + c0 + kCB <= p.N) {
+      // interior block: no per-store bounds checks (branches cost the exposed epilogue)
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int row = it * 4 + static_cast<int>(lane >> 3);
-      const int m = mrow0 + row;
-      const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
-      if (m < p.M && !(p.dbg_flags & 1)) {
-        uint8_t* dst = static_cast<uint8_t*>(p.out) + (static_cast<size_t>(m) * p.ldy + n) * (kF16 ? 2 : 4);
-        if (n + kPer <= p.N) {
-          *reinterpret_cast<uint4*>(dst) = v;
-        } else if (n < p.N) {
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-          for (int k = 0; k < kPer && n + k < p.N; ++k) {
-            if (kF16)
-              reinterpret_cast<uint16_t*>(dst)[k] = static_cast<uint16_t>(w[k >> 1] >> ((k & 1) * 16));
-            else
-              reinterpret_cast<uint32_t*>(dst)[k] = w[k];
+      for (int it = 0; it < 8; ++it) {
+        const int row = it * 4 + static_cast<int>(lane >> 3);
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
+        *reinterpret_cast<uint4*>(out0 + row * row_bytes) = v;
+      }
+    } else {
+#pragma unroll 1
+      for (int it = 0; it < 8; ++it) {
+        const int row = it * 4 + static_cast<int>(lane >> 3);
+        const int m = mrow0 + row;
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
+        if (m < p.M) {
+          uint8_t* dst = out0 + row * row_bytes;
+          if (n + kPer <= p.N) {
+            *reinterpret_cast<uint4*>(dst) = v;
+          } else if (n < p.N) {
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            for (int k = 0; k < kPer && n + k < p.N; ++k) {
+              if (kF16)
+                reinterpret_cast<uint16_t*>(dst)[k] = static_cast<uint16_t>(w[k >> 1] >> ((k & 1) * 16));
+              else
+                reinterpret_cast<uint32_t*>(dst)[k] = w[k];
+            }
           }
         }
       }

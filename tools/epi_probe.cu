@@ -1,0 +1,148 @@
+// Standalone timing of the K5p exposed-epilogue math (scales -> FP16 pack ->
+// smem transpose -> row stores) on register data, outside the big kernel:
+// 8 warps x 32 rows x 128 columns x 2 sub-tiles per CTA, 148 CTAs.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o epi_probe tools/epi_probe.cu
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ float i2f_small(int32_t acc, bool& ok) {
+  ok = static_cast<uint32_t>(acc + 0x400000) < 0x800000u;
+  return __fsub_rn(__int_as_float(acc + 0x4B400000), 12582912.0f);
+}
+
+template <int V, int W = 8>
+__global__ void __launch_bounds__(W * 32, 1) k_epi(const int32_t* __restrict__ accg, const float* __restrict__ s1g,
+                                                 __half* __restrict__ out, int ldy, int reps, int store) {
+  __shared__ __align__(16) float s_s1[256];
+  extern __shared__ __align__(16) uint8_t stg_dyn[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_s1[i] = s1g[i];
+  __syncthreads();
+  uint8_t* stg = stg_dyn + warp * 4096;
+  uint8_t* myrow = stg + lane * 128;
+  const uint32_t sw = lane & 7;
+  constexpr int kCols = 256 / (W / 4);
+  const int cbeg = (warp >> 2) * kCols, cend = cbeg + kCols;
+  const float rsm = 0.0123f + lane * 1e-4f;
+  const int mrow0 = blockIdx.x * 256 + (warp & 3) * 32;
+  uint32_t base = accg[threadIdx.x];
+  for (int rep = 0; rep < reps; ++rep) {
+    for (int sub = 0; sub < 2; ++sub) {
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 64) {
+#pragma unroll
+        for (int c16 = 0; c16 < 64; c16 += 16) {
+          uint32_t cur[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) cur[k] = base + (c0 + c16 + k) * 977u + sub;  // stand-in for TMEM data
+#pragma unroll
+          for (int c8 = 0; c8 < 16; c8 += 8) {
+            const int c1 = c16 + c8;
+            float y[8];
+            const float4 sa = *reinterpret_cast<const float4*>(s_s1 + c0 + c1);
+            const float4 sb = *reinterpret_cast<const float4*>(s_s1 + c0 + c1 + 4);
+            const float sv[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+            bool small = true;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              bool ok;
+              if (V & 8) { y[k] = static_cast<float>(cur[c8 + k] & 0xFFFF); ok = true; }
+              else if (V & 16) { y[k] = __int2float_rn(static_cast<int32_t>(cur[c8 + k]) >> 10); ok = true; }
+              else y[k] = i2f_small(static_cast<int32_t>(cur[c8 + k]) >> 10, ok);
+              small &= ok;
+            }
+            if (!(V & 1) && !(V & 16) && !__all_sync(0xffffffffu, small)) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) y[k] = __int2float_rn(static_cast<int32_t>(cur[c8 + k]) >> 10);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = __fmul_rn(__fmul_rn(y[k], rsm), sv[k]);
+            uint32_t h[4];
+            uint32_t tiny = 0;
+            float mn = 1.0f;
+            if (V & 16) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) mn = fminf(mn, fabsf(y[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (V & 4) {
+                h[k] = __float_as_uint(y[2 * k]) ^ (__float_as_uint(y[2 * k + 1]) << 1);
+              } else {
+                const __half2 hh = __floats2half2_rn(y[2 * k], y[2 * k + 1]);
+                h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+              }
+              if (!(V & 16))
+                tiny |= static_cast<uint32_t>((h[k] & 0x7FFFu) == 1u) | static_cast<uint32_t>((h[k] & 0x7FFF0000u) == 0x10000u);
+            }
+            if (V & 16) tiny = mn < 0x1p-24f;
+            if (V & 32) {  // branch-free: the flush select on every pair
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t lo = (__float_as_uint(y[2 * k]) >> 16) & 0x8000u;
+                const uint32_t hi = __float_as_uint(y[2 * k + 1]) & 0x80000000u;
+                uint32_t u = h[k];
+                u = fabsf(y[2 * k]) < 0x1p-24f ? ((u & 0xFFFF0000u) | lo) : u;
+                u = fabsf(y[2 * k + 1]) < 0x1p-24f ? ((u & 0x0000FFFFu) | hi) : u;
+                h[k] = u;
+              }
+            } else if (!(V & 2) && tiny) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                uint32_t u = h[k];
+                if (fabsf(y[2 * k]) < 0x1p-24f) u = (u & 0xFFFF0000u) | ((__float_as_uint(y[2 * k]) >> 16) & 0x8000u);
+                if (fabsf(y[2 * k + 1]) < 0x1p-24f) u = (u & 0x0000FFFFu) | (__float_as_uint(y[2 * k + 1]) & 0x80000000u);
+                h[k] = u;
+              }
+            }
+            *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
+          }
+        }
+        __syncwarp();
+        const int ch = lane & 7;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int row = it * 4 + (lane >> 3);
+          const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
+          if (store) *reinterpret_cast<uint4*>(out + static_cast<size_t>(mrow0 + row) * ldy + c0 + ch * 8) = v;
+          else if (v.x == 0x12345678u) out[0] = __float2half(1.0f);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+int main() {
+  int32_t* acc; float* s1; __half* out;
+  cudaMalloc(&acc, 1024 * 4); cudaMalloc(&s1, 256 * 4); cudaMalloc(&out, size_t(148) * 256 * 256 * 2);
+  cudaMemset(acc, 1, 4096); cudaMemset(s1, 0, 1024);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  auto run = [&](auto kern, const char* name, int thr = 256) {
+    const int smem = thr / 32 * 4096;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kern<<<148, thr, smem>>>(acc, s1, out, 256, 1, 1);
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    kern<<<148, thr, smem>>>(acc, s1, out, 256, 10, 1);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("%-28s %.2f us per tile epilogue (%s)\n", name, ms * 1e3 / 10, cudaGetErrorString(cudaGetLastError()));
+  };
+  run(k_epi<0>, "full");
+  run(k_epi<16>, "I2F + min-abs tiny");
+  run(k_epi<48>, "I2F + branch-free flush");
+  run(k_epi<48, 16>, "branch-free, 16 warps", 512);
+  run(k_epi<0, 16>, "full, 16 warps", 512);
+  run(k_epi<48, 4>, "branch-free, 4 warps", 128);
+  run(k_epi<1>, "no vote");
+  run(k_epi<2>, "no tiny check");
+  run(k_epi<3>, "no vote, no tiny");
+  run(k_epi<4>, "no F2FP");
+  run(k_epi<7>, "no vote/tiny/F2FP");
+  run(k_epi<15>, "no vote/tiny/F2FP/magic");
+  return 0;
+}
