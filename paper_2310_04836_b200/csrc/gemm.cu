@@ -607,11 +607,11 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
     // two token sub-tiles per CTA (512-token pair tiles) from 512 tokens, with
     // stream-K balancing the tiles; mode bit 17 keeps one (256-token tiles)
     // two sub-tiles pay an exposed epilogue per segment for a ~30 % faster
-    // main loop: worth it from ~100 k-blocks of 512-token tiles per pair
-    // (tools/decode_sweep.py: OPT-30B fc1 / fc2 at M >= 1024 and fc2 at 512
-    // gain 8-16 %, q at 2048 and 4096^2 shapes lose)
+    // main loop: worth it from ~25 k-blocks of 512-token tiles per pair
+    // (tools/decode_sweep.py --s2 / --s1, after the branch-free epilogue:
+    // q 7168^2 at M = 1024 / 2048 45 / 84 vs 54 / 91 us, 4096^2 at 1024 30 vs 23)
     const long long t512 = ((M + 511) / 512) * static_cast<long long>((N + 255) / 256);
-    const bool s2_pays = t512 * kblocks >= 100LL * pairs;
+    const bool s2_pays = t512 * kblocks >= 25LL * pairs;
     pl.pair_sub = (sk && pl.pair_tn == 256 && M >= 512 && (s2_pays || (g_decode_mode & 0x40000000)) &&
                    (g_decode_mode & 0x20000) == 0 && dgq_prefill2_smem_bytes(cb, 2) <= 232448) ? 2 : 1;
     pl.bn = 256 * pl.pair_sub;

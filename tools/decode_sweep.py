@@ -17,6 +17,8 @@ if "--pair" in sys.argv:  # route M >= 33 to the CTA-pair prefill kernel (K5p)
     _mode |= 0x400
 if "--dec64" in sys.argv:  # K5d (decode kernel) up to 64 tokens
     _mode |= 0x10000000
+if "--s2" in sys.argv:  # K5p with two token sub-tiles whenever M >= 512
+    _mode |= 0x40000000
 if "--s1" in sys.argv:  # K5p with one token sub-tile per CTA (256-token pair tiles)
     _mode |= 0x20000
 _cap = [int(a.split("=")[1]) for a in sys.argv[1:] if a.startswith("--cap=")]
