@@ -300,7 +300,7 @@ __device__ __forceinline__ size_t part_off(int c16, int v, int row) {
 // whole 128-byte row segments (a lane-per-row 16-byte store touched 32 lines
 // per instruction; tools/pf_trace.py measured an 11 us epilogue that way, and
 // a TMA store per 64 columns serialises on its issue latency).
-template <int TN, bool kF16>
+template <int TN, bool kF16, bool kFlush>
 __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbase, float rsm, const float* s_s1,
                                            const float* s_bias, uint8_t* stg, int mrow0, int nbase, int cbeg,
                                            int cend) {
@@ -359,8 +359,10 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
               // zero; selects, not a branch (tools/epi_probe.cu: the branch cost 2x)
               const uint32_t lo = (__float_as_uint(y[2 * k]) >> 16) & 0x8000u;
               const uint32_t hi = __float_as_uint(y[2 * k + 1]) & 0x80000000u;
-              u = fabsf(y[2 * k]) < 0x1p-24f ? ((u & 0xFFFF0000u) | lo) : u;
-              u = fabsf(y[2 * k + 1]) < 0x1p-24f ? ((u & 0x0000FFFFu) | hi) : u;
+              if (kFlush) {
+                u = fabsf(y[2 * k]) < 0x1p-24f ? ((u & 0xFFFF0000u) | lo) : u;
+                u = fabsf(y[2 * k + 1]) < 0x1p-24f ? ((u & 0x0000FFFFu) | hi) : u;
+              }
               h[k] = u;
             }
             *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
@@ -870,10 +872,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
         if (m0 >= p.M) continue;  // a token quarter past M: nothing to store
         if (S == 2 && p.out && p.vec_ok && !p.acc_out) {
           if constexpr (S == 2) {
-            if (p.out_f16)
-              epi_direct<TN, true>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
-            else
-              epi_direct<TN, false>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+            // No value of this warp's rows can land in fp16_round's flush range
+            // (0 < |y| < 2^-24) when rs * min(s1) >= 2^-24: |acc| >= 1 for every
+            // non-zero accumulator and RN is monotonic (no bias, FP32 scale mode)
+            float s1min = 3.0e38f;
+            for (int c = cbeg + static_cast<int>(lane); c < cend; c += 32) s1min = fminf(s1min, s_s1[c]);
+            for (int o = 16; o > 0; o >>= 1) s1min = fminf(s1min, __shfl_xor_sync(0xffffffffu, s1min, o));
+            const bool safe = !p.bias && !p.fp16_mode && __fmul_rn(rsm, s1min) >= 0x1p-24f;
+            if (p.out_f16) {
+              if (__all_sync(0xffffffffu, safe))
+                epi_direct<TN, true, false>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+              else
+                epi_direct<TN, true, true>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+            } else {
+              epi_direct<TN, false, true>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+            }
           }
         } else if (S == 1 && p.tma_out && !p.acc_out) {
           if constexpr (S == 1) {

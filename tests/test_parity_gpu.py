@@ -603,3 +603,30 @@ def test_gpu_calibration_errors(cuda):
         dgq.calibrate(torch.zeros(4, 64, device="cuda"))  # all-zero calibration: threshold not positive
     with pytest.raises(dgq.InvalidArgument):
         dgq.calibrate(torch.ones(4, 64, device="cuda"), percentile=1.0)
+
+
+@pytest.mark.parametrize("s1_scale", [1e-9, 1.0])
+def test_prefill_fp16_flush_range(cuda, port, s1_scale):
+    # outputs around fp16_round's flush band (0 < |y| < 2^-24 -> signed zero,
+    # proj/src/quant.cpp:33-35) through the two-sub-tile kernel's epilogue: tiny
+    # per-channel scales force the flush path, normal ones let it be skipped
+    import ctypes
+
+    M, h, o, g = 1024, 1024, 512, 128
+    L = oracle.random_layer(h, o, g, seed=17)
+    L.s1 = (L.s1 * np.float32(s1_scale)).astype(np.float32)
+    X = port.gen_synthetic(M, h, 23, 3, 50.0, 3)
+    out, *_ = port.dgq_forward(X, L)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    lib = dgq.lib()
+    lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    lib.dgq_debug_set_decode(1 | 0x400 | 0x40000000)  # K5p with two token sub-tiles
+    try:
+        codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+        y16 = CL.linear(codes, drs, out_dtype=torch.float16)
+    finally:
+        lib.dgq_debug_set_decode(1)
+    ref = port.fp16_round_array(out).astype(np.float16)
+    assert np.array_equal(y16.cpu().numpy().view(np.uint16), ref.view(np.uint16))
+    if s1_scale < 1e-6:
+        assert (np.abs(out) < 2.0 ** -24).any() and (out != 0).any()

@@ -78,7 +78,20 @@ __global__ void __launch_bounds__(W * 32, 1) k_epi(const int32_t* __restrict__ a
                 tiny |= static_cast<uint32_t>((h[k] & 0x7FFFu) == 1u) | static_cast<uint32_t>((h[k] & 0x7FFF0000u) == 0x10000u);
             }
             if (V & 16) tiny = mn < 0x1p-24f;
-            if (V & 32) {  // branch-free: the flush select on every pair
+            if (V & 64) {  // min-abs per 8 values, one warp vote, rare uniform fix-up
+              float m8 = fabsf(y[0]);
+#pragma unroll
+              for (int k = 1; k < 8; ++k) m8 = fminf(m8, fabsf(y[k]));
+              if (__any_sync(0xffffffffu, m8 < 0x1p-24f)) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  uint32_t u = h[k];
+                  if (fabsf(y[2 * k]) < 0x1p-24f) u = (u & 0xFFFF0000u) | ((__float_as_uint(y[2 * k]) >> 16) & 0x8000u);
+                  if (fabsf(y[2 * k + 1]) < 0x1p-24f) u = (u & 0x0000FFFFu) | (__float_as_uint(y[2 * k + 1]) & 0x80000000u);
+                  h[k] = u;
+                }
+              }
+            } else if (V & 32) {  // branch-free: the flush select on every pair
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const uint32_t lo = (__float_as_uint(y[2 * k]) >> 16) & 0x8000u;
@@ -135,6 +148,8 @@ int main() {
   run(k_epi<0>, "full");
   run(k_epi<16>, "I2F + min-abs tiny");
   run(k_epi<48>, "I2F + branch-free flush");
+  run(k_epi<16 + 64>, "I2F + min/any-vote flush");
+  run(k_epi<16 + 2>, "I2F + no flush (floor)");
   run(k_epi<48, 16>, "branch-free, 16 warps", 512);
   run(k_epi<0, 16>, "full, 16 warps", 512);
   run(k_epi<48, 4>, "branch-free, 4 warps", 128);
