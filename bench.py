@@ -416,9 +416,9 @@ def decode_k5_streaming(layer, M, device, world, group):
 
 def measure_int8_peak(device):
     """Dense INT8 tensor throughput of this GPU: cuBLASLt (torch._int_mm), the
-    best of 10 CUDA-event timings after warm-up on three shapes (8192^3, the
-    OPT-30B fc1 shape, 4096x8192x8192) — a burst figure like MEASURED_PEAKS.json's
-    bf16 one.  None if the library path is missing."""
+    best of 6 replays of a CUDA graph of 5 back-to-back calls on each of three
+    shapes (8192^3, the OPT-30B fc1 shape, 4096x8192x8192) — a burst figure
+    like MEASURED_PEAKS.json's bf16 one.  None if the library path is missing."""
     import torch
 
     try:
@@ -428,15 +428,16 @@ def measure_int8_peak(device):
             b = torch.randint(-127, 128, (k, n), dtype=torch.int8, device=device)
             for _ in range(3):
                 torch._int_mm(a, b)
+            g = _graph_of(lambda: [torch._int_mm(a, b) for _ in range(5)])  # launch overhead amortised
             best = 1e30
-            for _ in range(10):
+            for _ in range(6):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                torch._int_mm(a, b)
+                g.replay()
                 e1.record()
                 e1.synchronize()
-                best = min(best, e0.elapsed_time(e1) * 1e-3)
-            del a, b
+                best = min(best, e0.elapsed_time(e1) * 1e-3 / 5)
+            del a, b, g
             top = max(top, 2.0 * m * k * n / best / 1e12)
         return top
     except Exception:  # noqa: BLE001
