@@ -622,7 +622,7 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     ms = make_tmap(&tmX, dXq, M, k_pad, ldq, 128u);
     if (ms != DGQ_OK) return ms;
     p.chunk_stride = p.chunk_bytes;
-    p.dbg_flags = (dgq_debug_decode_mode() >> 18) & 7;  // tools: mode bits 18-20
+    p.dbg_flags = (dgq_debug_decode_mode() >> 18) & 31;  // tools: mode bits 18-22
     if (pl.stream_k) {
       if (!ws) return fail(DGQ_EINVAL, "stream-K prefill kernel needs a workspace");
       p.stream_k = 1;

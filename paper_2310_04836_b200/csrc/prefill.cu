@@ -870,8 +870,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
         const float rsm = s_rs[sub * 128 + mrow];
         if (et == 0 && tl < 8) pf_stamp(p, 9, 512 + 4 * tl + sub);
         if (m0 >= p.M) continue;  // a token quarter past M: nothing to store
-        if (S == 2 && p.out && p.vec_ok && !p.acc_out) {
-          if constexpr (S == 2) {
+        if (p.out && p.vec_ok && !p.acc_out && !(S == 1 && (p.dbg_flags & 16))) {  // tools: 16 = S=1 TMA epilogue
+          {
             // No value of this warp's rows can land in fp16_round's flush range
             // (0 < |y| < 2^-24) when rs * min(s1) >= 2^-24: |acc| >= 1 for every
             // non-zero accumulator and RN is monotonic (no bias, FP32 scale mode)

@@ -19,6 +19,8 @@ if "--dec64" in sys.argv:  # K5d (decode kernel) up to 64 tokens
     _mode |= 0x10000000
 if "--s2" in sys.argv:  # K5p with two token sub-tiles whenever M >= 512
     _mode |= 0x40000000
+if "--tmaepi" in sys.argv:  # K5p 256-token tiles keep the TMA-store epilogue
+    _mode |= 0x400000
 if "--s1" in sys.argv:  # K5p with one token sub-tile per CTA (256-token pair tiles)
     _mode |= 0x20000
 _cap = [int(a.split("=")[1]) for a in sys.argv[1:] if a.startswith("--cap=")]
