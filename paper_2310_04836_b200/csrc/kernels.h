@@ -58,7 +58,7 @@ struct DgqGemmParams {
   uint32_t* counters;
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
   int stream_k;             // K5p: stream-K over (tile, k-block) units (ws / counters = pair slots / flags)
-  int dbg_flags;            // tools only (K5p): 1 = epilogue skips its global stores, 2 = also its math, 4 = math only
+  int dbg_flags;            // tools only (K5p): 16 = 256-token tiles keep the TMA-store epilogue
 };
 
 // K5d (decode.cu): stream-K over (weight tile, k-block) units, (code - ZP) as
