@@ -36,7 +36,7 @@ n = int((b[0] > 0).sum())
 t0 = b[:5, :n][b[:5, :n] > 0].min()
 r = lambda v: (v - t0) / 1e3 if v > 0 else float("nan")  # noqa: E731
 print(" kb | issue   full  bempty  dq-done | mma    | A-issue  loop#")
-for i in list(range(0, 4)) + list(range(50, 66)):
+for i in list(range(20, 30)):
     if i < n:
         print(f"{i:3d} | {r(b[1][i]):6.2f} {r(b[2][i]):6.2f} {r(b[3][i]):6.2f} {r(b[4][i]):6.2f} | {r(b[0][i]):6.2f} | "
               f"{r(b[5][i]):6.2f} {int(b[6][i]) if b[6][i] else 0:8d}")
