@@ -110,9 +110,13 @@ __global__ void __launch_bounds__(W * 32, 1) k_epi(const int32_t* __restrict__ a
                 h[k] = u;
               }
             }
-            *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
+            if (V & 128)
+              *reinterpret_cast<uint4*>(out + static_cast<size_t>(mrow0 + lane) * ldy + c0 + c1) = make_uint4(h[0], h[1], h[2], h[3]);
+            else
+              *reinterpret_cast<uint4*>(myrow + (((c1 / 8) ^ sw) << 4)) = make_uint4(h[0], h[1], h[2], h[3]);
           }
         }
+        if (V & 128) continue;
         __syncwarp();
         const int ch = lane & 7;
 #pragma unroll
@@ -150,6 +154,7 @@ int main() {
   run(k_epi<48>, "I2F + branch-free flush");
   run(k_epi<16 + 64>, "I2F + min/any-vote flush");
   run(k_epi<16 + 2>, "I2F + no flush (floor)");
+  run(k_epi<16 + 2 + 128>, "floor, direct 16B stores");
   run(k_epi<48, 16>, "branch-free, 16 warps", 512);
   run(k_epi<0, 16>, "full, 16 warps", 512);
   run(k_epi<48, 4>, "branch-free, 4 warps", 128);
