@@ -839,13 +839,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
         // int32).  An owner segment is always its pair's LAST, so the Xq / B
         // rings are idle: each contributor's 128-row partial (128 KB) comes in
         // with one bulk copy instead of per-thread L2 round trips.
+        auto load_part = [&](int c, int s) {
+          mbar_arrive_expect_tx(fbar, static_cast<uint32_t>(kSub * 4));
+          bulk_load(sA, p.ws + (static_cast<size_t>(cid + c) * 2 + rank) * kSlot + s * kSub,
+                    static_cast<uint32_t>(kSub * 4), fbar);
+        };
 #pragma unroll 1
         for (int c = 1; c <= npart; ++c) {
-          const int32_t* part = p.ws + (static_cast<size_t>(cid + c) * 2 + rank) * kSlot + sub * kSub;
-          if (et == 0) {
-            mbar_arrive_expect_tx(fbar, static_cast<uint32_t>(kSub * 4));
-            bulk_load(sA, part, static_cast<uint32_t>(kSub * 4), fbar);
-          }
+          // sub-tile 1's first partial was prefetched while sub-tile 0's rows drained
+          if (et == 0 && !(sub > 0 && c == 1)) load_part(c, sub);
           wait_local(fbar, fphase, 10);
           fphase ^= 1u;
           const int32_t* sp = reinterpret_cast<const int32_t*>(sA);
@@ -866,6 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
           }
           tmem_st_wait();
           named_bar(2, kEpiThreads);  // every row read before the next partial overwrites the buffer
+          if (et == 0 && c == npart && sub + 1 < S) load_part(1, sub + 1);
         }
         const float rsm = s_rs[sub * 128 + mrow];
         if (et == 0 && tl < 8) pf_stamp(p, 9, 512 + 4 * tl + sub);
