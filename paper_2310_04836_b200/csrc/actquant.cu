@@ -602,7 +602,10 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     if (C8 <= 512) DGQ_AQ3(256, 2)
     if (C8 <= 1024) DGQ_AQ3(256, 4)
     if (C8 <= 2048) DGQ_AQ3(512, 4)
-    DGQ_AQ3(512, 8)
+    // one row per CTA fills the smem (114 KB double-buffered at K = 28672 FP16):
+    // 32 warps instead of 16 hide the per-row latency (fc2 input 69.7 -> 65.5 us;
+    // the same widening slowed 7168-wide rows, tools/k1_time.py)
+    DGQ_AQ3(1024, 4)
 #undef DGQ_AQ3
   }
 #define DGQ_AQ(T_, V_, CL_)                                                                                    \
