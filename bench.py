@@ -202,11 +202,15 @@ class OptLayer:
         self.world, self.device, self.M_max = world, device, M_max
         qkv_k = None
         self.lin = {}
+        self.host = {}  # host DgqLayers (reference layout) for the post-run self-check
+        self.rank = rank
         for i, (name, K, N) in enumerate(OPT30B):
             L = tiled_layer(K, N, seed=100 + i, k_vec=qkv_k if name in ("k", "v") else None)
             if name == "q":
                 qkv_k = L.k  # q/k/v share the input and its smoothing vector
             self.lin[name] = ColumnParallelLinear(L, rank, world, device, group)
+            if name in ("fc1", "fc2"):
+                self.host[name] = L
         f16 = torch.float16
         dev = device
         self.x = torch.empty(M_max, 7168, dtype=torch.float32, device=dev)
@@ -285,6 +289,39 @@ class OptLayer:
         self._k5("fc2", self.codes["fc2"], self.rs["fc2"], M)
         self._gather("fc2", M)
         return self.y["fc2"][:M]
+
+
+def verify_step(layer, M, n_rows=8):
+    """Self-check of the timed work: sampled rows of this rank's fc1 and fc2
+    outputs from the last step, against the reference's own dgq_forward
+    (oracle/_ref, proj/src/kernel.cpp:144-153) on the same FP16 inputs
+    (the gathered out / fc1 activations) and the rank's column shard.  The FP16
+    output must equal fp16_round(reference FP32 output) bit for bit."""
+    import numpy as np
+
+    import oracle
+    from paper_2310_04836_b200.parallel import gathered_to_full, shard_layer
+
+    torch = __import__("torch")
+    torch.cuda.synchronize()
+    be = oracle.best()
+    rows = np.unique(np.concatenate([[0, 255, 256, 511, M // 2, M - 1],
+                                     np.random.default_rng(7).integers(0, M, n_rows - 6)]))
+    res = {"rows": rows.tolist(), "oracle": be.kind}
+    ok = True
+    for name, src in (("fc1", "out"), ("fc2", "fc1")):
+        g = layer.y[src][:M].unsqueeze(0) if layer.world == 1 else layer.g[src][:, :M]
+        x = gathered_to_full(g)[torch.from_numpy(rows).to(g.device)].float().cpu().numpy()
+        S = shard_layer(layer.host[name], layer.rank, layer.world) if layer.world > 1 else layer.host[name]
+        out = be.dgq_forward(x, _oracle_layer(S), None, 0)[0] if be.kind == "reference" \
+            else be.dgq_forward(x, _oracle_layer(S))[0]
+        want = oracle.fp16_round_np(out).astype(np.float16).view(np.uint16)
+        got = layer.y[name][torch.from_numpy(rows).to(g.device)].cpu().numpy().view(np.uint16)
+        same = bool(np.array_equal(got, want))
+        res[name] = {"bit_exact_fp16": same, "mismatches": int((got != want).sum()), "elements": int(got.size)}
+        ok = ok and same
+    res["ok"] = ok
+    return res
 
 
 def timed_steps(layer, M, steps, warmup, flush, sync_all, e2e=None):
@@ -582,6 +619,12 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # ---- self-check of the timed outputs (after the timed region) ---------------------------
+    try:
+        verified = verify_step(layer, SEQ)
+    except Exception as e:  # noqa: BLE001  (oracle not built on this box)
+        verified = {"ok": None, "error": f"{type(e).__name__}: {e}"}
+
     # ---- e2e through the public API with host buffers ---------------------------------------
     out_host = torch.empty(SEQ, layer.lin["fc2"].shard, dtype=torch.float16).pin_memory()
     e2e_times = timed_steps(layer, SEQ, args.steps, 1, flush, sync_all, e2e=(x_host, out_host))
@@ -658,6 +701,8 @@ def run_ours(args):
                                       f"frac {k5_tops / 4500:.3f}",
                          "traffic": traffic},
             "cpu_baseline": cpu,
+            "verified": verified.get("ok"),
+            "verification": verified,
             "clocks": clk,
             "detail": detail,
         }

@@ -186,6 +186,29 @@ dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW
 dgq_status dgq_calibrate(const float* dX, size_t rows, size_t h, size_t ldx, float percentile, int fp16_scales,
                          float* k_out, float* threshold_out, float* act_scale_out, void* stream);
 
+/* ---- offline quantiser: two-phase grid search -----------
+ * The step that produces a layer's S2 / ZP / s1 / codes from FP32 weights,
+ * bit-exact with the reference (FP64 objectives accumulated in the
+ * reference's fixed order, smallest-alpha tie-break).  Device arrays:
+ * dW [h x o] f32 row-major; dX, dXhat [b x h] f32 = the smoothed calibration
+ * rows and their quantise-dequantise (SearchConfig::calib_X and X_hat).
+ * alpha_grid is a HOST array searched in the given order.  Stream-ordered
+ * (scratch from the device's stream-ordered pool: phase 1 needs
+ * (h/g)*o*(8*b + 8*n_alpha + 8) bytes); evals (host, may be NULL) =
+ * objective evaluations.  Errors mirror SearchConfig::validate. */
+/* replaces dgq::phase1_search, proj/src/search.cpp:83-163: per (group, column)
+ * S' [h/g x o] f32, ZP int32, winning objective f32 and alpha f32 */
+dgq_status dgq_phase1_search(const float* dW, size_t h, size_t o, const float* dX, const float* dXhat, size_t b,
+                             size_t g, int n_bits, const float* alpha_grid, size_t n_alpha, float* dSprime,
+                             int32_t* dZp, float* dErr, float* dAlpha, uint64_t* evals, void* stream);
+/* replaces dgq::phase2_search, proj/src/search.cpp:252-326: from phase 1's S'
+ * and ZP, per column s1 [o] f32, S2 [h/g x o] int8, codes [h x o] int32,
+ * objective [o] f64 and winning alpha [o] f32 */
+dgq_status dgq_phase2_search(const float* dW, size_t h, size_t o, const float* dX, const float* dXhat, size_t b,
+                             size_t g, const float* dSprime, const int32_t* dZp, const float* alpha_grid,
+                             size_t n_alpha, float* dS1, int8_t* dS2, int32_t* dCodes, double* dColErr,
+                             float* dColAlpha, uint64_t* evals, void* stream);
+
 /* ---- host-buffer API: the reference's calling convention --------------------
  * Host arrays in (reference layouts), host arrays out; each call uploads,
  * runs the CUDA kernels on a per-thread stream of the CURRENT device and

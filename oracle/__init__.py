@@ -89,6 +89,10 @@ class _Backend:
             f("dgq_forward").argtypes = ([_vp, _sz, _sz, _sz, _sz, C.c_int, C.c_float] + [_vp] * 6
                                          + [C.c_int] + [_vp] * 5)
             f("dgq_to_bytes").argtypes = [_sz, _sz, _sz, C.c_int, C.c_float] + [_vp] * 7
+            f("phase1_search").argtypes = ([_vp, _sz, _sz, _vp, _vp, _sz, _sz, C.c_int, _vp, _sz, C.c_int]
+                                           + [_vp] * 5)
+            f("phase2_search").argtypes = ([_vp, _sz, _sz, _vp, _vp, _sz, _sz, C.c_int, _vp, _vp, _vp, _sz,
+                                            C.c_int] + [_vp] * 6)
         else:
             f("int8_gemm").argtypes = [_vp, _vp, _sz, _sz, _sz, _vp, _vp]
             f("validate_layer").argtypes = ([_sz, _sz, _sz, C.c_int, C.c_float] + [_vp] * 5
@@ -212,6 +216,40 @@ class _Backend:
         self._check(st)
         return out, w, q, rs, int(mx[0])
 
+    # ---- offline quantiser (reference only): search.cpp:83-163, 252-326 ----
+    def phase1_search(self, W, X, Xhat, g, grid, n_bits=4, threads=0):
+        """Returns (s_prime f32 [n_g,o], zp i32, err f32, alpha f32, evals)."""
+        assert self.pfx == "ref_"
+        W, X, Xhat = (np.ascontiguousarray(a, np.float32) for a in (W, X, Xhat))
+        grid = np.ascontiguousarray(grid, np.float32)
+        h, o = W.shape
+        ng = h // g
+        sp, er, al = (np.empty((ng, o), np.float32) for _ in range(3))
+        zp = np.empty((ng, o), np.int32)
+        ev = np.zeros(1, np.uint64)
+        self._check(self._f("phase1_search")(_p(W), h, o, _p(X), _p(Xhat), X.shape[0], g, n_bits, _p(grid),
+                                             grid.size, threads, _p(sp), _p(zp), _p(er), _p(al), _p(ev)))
+        return sp, zp, er, al, int(ev[0])
+
+    def phase2_search(self, W, X, Xhat, g, s_prime, zp, grid, n_bits=4, threads=0):
+        """Returns (s1 f32 [o], s2 i8 [n_g,o], codes i32 [h,o], col_err f64 [o], col_alpha f32 [o], evals)."""
+        assert self.pfx == "ref_"
+        W, X, Xhat = (np.ascontiguousarray(a, np.float32) for a in (W, X, Xhat))
+        s_prime = np.ascontiguousarray(s_prime, np.float32)
+        zp = np.ascontiguousarray(zp, np.int32)
+        grid = np.ascontiguousarray(grid, np.float32)
+        h, o = W.shape
+        ng = h // g
+        s1, ca = np.empty(o, np.float32), np.empty(o, np.float32)
+        s2 = np.empty((ng, o), np.int8)
+        codes = np.empty((h, o), np.int32)
+        ce = np.empty(o, np.float64)
+        ev = np.zeros(1, np.uint64)
+        self._check(self._f("phase2_search")(_p(W), h, o, _p(X), _p(Xhat), X.shape[0], g, n_bits, _p(s_prime),
+                                             _p(zp), _p(grid), grid.size, threads, _p(s1), _p(s2), _p(codes),
+                                             _p(ce), _p(ca), _p(ev)))
+        return s1, s2, codes, ce, ca, int(ev[0])
+
     def dgq_to_bytes(self, L: Layer) -> bytes:
         assert self.pfx == "ref_"
         n = C.c_size_t()
@@ -290,6 +328,19 @@ def unpack_u4(packed: np.ndarray, count: int) -> np.ndarray:
     out[0::2] = p & 0x0F
     out[1::2] = p >> 4
     return out[:count]
+
+
+def fp16_round_np(x) -> np.ndarray:
+    """Vectorised fp16_round (proj/src/quant.cpp:9-58): IEEE binary16
+    round-to-nearest-even, except that |x| in [2^-25, 2^-24) flushes to a signed
+    zero (the reference's `exp >= -24` subnormal branch starts at 2^-24; RNE
+    would round (2^-25, 2^-24) up to 2^-24).  Pinned against the scalar
+    reference by tests/test_oracle.py."""
+    x = np.asarray(x, np.float32)
+    y = x.astype(np.float16).astype(np.float32)
+    a = np.abs(x)
+    band = (a >= np.float32(2.0 ** -25)) & (a < np.float32(2.0 ** -24))
+    return np.where(band, np.copysign(np.float32(0.0), x), y).astype(np.float32)
 
 
 def clip_bounds(s2: np.ndarray, zp: np.ndarray):

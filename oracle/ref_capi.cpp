@@ -215,4 +215,55 @@ int ref_dgq_to_bytes(size_t h, size_t o, size_t g, int mode, float act_scale,
   });
 }
 
+// Two-phase grid search (search.cpp:83-163, 252-326) on plain buffers.
+// W [h x o] f32, X / X_hat [b x h] f32 (smoothed calibration rows and their
+// quantise-dequantise), grids in the caller's order.
+int ref_phase1_search(const float* W, size_t h, size_t o, const float* X, const float* Xhat, size_t b,
+                      size_t g, int n_bits, const float* grid1, size_t n1, int threads, float* s_prime,
+                      int32_t* zp, float* err, float* alpha, uint64_t* evals) {
+  return guarded([&] {
+    dgq::SearchConfig cfg;
+    cfg.group_size = g;
+    cfg.n_bits_w = n_bits;
+    cfg.alpha_grid_phase1.assign(grid1, grid1 + n1);
+    cfg.calib_X = tensor_from(dgq::Dtype::kF32, b, h, X);
+    cfg.threads = threads;
+    dgq::GroupParams gp =
+        dgq::phase1_search(tensor_from(dgq::Dtype::kF32, h, o, W), cfg, tensor_from(dgq::Dtype::kF32, b, h, Xhat));
+    const size_t n = gp.s_prime.size();
+    std::memcpy(s_prime, gp.s_prime.f32_data(), 4 * n);
+    std::memcpy(zp, gp.zp.i32_data(), 4 * n);
+    std::memcpy(err, gp.err.f32_data(), 4 * n);
+    std::memcpy(alpha, gp.alpha.f32_data(), 4 * n);
+    *evals = gp.objective_evals;
+  });
+}
+
+int ref_phase2_search(const float* W, size_t h, size_t o, const float* X, const float* Xhat, size_t b,
+                      size_t g, int n_bits, const float* s_prime, const int32_t* zp, const float* grid2,
+                      size_t n2, int threads, float* s1, int8_t* s2, int32_t* codes, double* col_err,
+                      float* col_alpha, uint64_t* evals) {
+  return guarded([&] {
+    dgq::SearchConfig cfg;
+    cfg.group_size = g;
+    cfg.n_bits_w = n_bits;
+    cfg.alpha_grid_phase2.assign(grid2, grid2 + n2);
+    cfg.calib_X = tensor_from(dgq::Dtype::kF32, b, h, X);
+    cfg.threads = threads;
+    dgq::GroupParams gp;
+    gp.group_size = g;
+    gp.n_bits = n_bits;
+    gp.s_prime = tensor_from(dgq::Dtype::kF32, h / g, o, s_prime);
+    gp.zp = tensor_from(dgq::Dtype::kI32, h / g, o, zp);
+    dgq::DualSearchResult r = dgq::phase2_search(tensor_from(dgq::Dtype::kF32, h, o, W), gp, cfg,
+                                                 tensor_from(dgq::Dtype::kF32, b, h, Xhat));
+    std::memcpy(s1, r.params.s1.data(), 4 * o);
+    std::memcpy(s2, r.params.s2.i8_data(), r.params.s2.size());
+    std::memcpy(codes, r.codes.i32_data(), 4 * r.codes.size());
+    std::memcpy(col_err, r.col_err.data(), 8 * o);
+    std::memcpy(col_alpha, r.col_alpha.data(), 4 * o);
+    *evals = r.objective_evals;
+  });
+}
+
 }  // extern "C"

@@ -9,7 +9,8 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdgq_b200.so")
+# DGQ_B200_LIB: tools-only override (A/B of two builds of this library)
+LIB_PATH = os.environ.get("DGQ_B200_LIB") or os.path.join(_PKG, "libdgq_b200.so")
 
 _vp, _sz, _i, _f = C.c_void_p, C.c_size_t, C.c_int, C.c_float
 
@@ -83,6 +84,10 @@ _SIGS = {
     "dgq_linear_multi": (_i, [C.POINTER(_vp), _i, _vp, _sz, _vp, _sz, C.POINTER(_vp), _i, C.POINTER(_vp),
                               C.POINTER(_sz), _vp, _sz, _vp]),
     "dgq_linear_multi_workspace_bytes": (_sz, [C.POINTER(_vp), _i, _sz]),
+    "dgq_phase1_search": (_i, [_vp, _sz, _sz, _vp, _vp, _sz, _sz, _i, _vp, _sz, _vp, _vp, _vp, _vp,
+                               C.POINTER(C.c_uint64), _vp]),
+    "dgq_phase2_search": (_i, [_vp, _sz, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp,
+                               C.POINTER(C.c_uint64), _vp]),
     # host-buffer API (the reference's calling convention)
     "dgq_host_quantize_activations": (_i, [_vp, _sz, _sz, _vp, _i, _f, _vp, _vp]),
     "dgq_host_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp]),
@@ -111,6 +116,8 @@ def lib():
                                   "(there is no CPU fallback)")
             L = C.CDLL(LIB_PATH)
             for name, (res, args) in _SIGS.items():
+                if os.environ.get("DGQ_B200_LIB") and not hasattr(L, name):
+                    continue  # an older build under A/B
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args

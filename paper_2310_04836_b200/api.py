@@ -163,7 +163,6 @@ class CudaLayer:
         self.info = info
         self.h, self.o, self.k_pad = info.h, info.o, info.k_pad
         self.mode, self.act_scale, self.fused = info.mode, info.act_scale, bool(info.fused)
-        self._ws = None
 
     @classmethod
     def from_dgq1(cls, data: bytes, device=None, col_begin: int = 0, col_end: int | None = None) -> "CudaLayer":
@@ -197,12 +196,13 @@ class CudaLayer:
         return dict(token_tile=v[0].value, weight_tiles=v[1].value, k_splits=v[2].value, ctas=v[3].value)
 
     def workspace(self, M: int) -> torch.Tensor | None:
+        """A zeroed split-K workspace for M tokens that the caller owns (pass it to
+        linear(); use one per stream).  Without one, linear() lets the library
+        use the layer's internal workspace for the current stream."""
         need = lib().dgq_linear_workspace_bytes(self._h, M)
         if need == 0:
             return None
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.zeros(need, dtype=torch.uint8, device=f"cuda:{self.device}")
-        return self._ws
+        return torch.zeros(need, dtype=torch.uint8, device=f"cuda:{self.device}")
 
     # K1
     def quantize_act(self, x: torch.Tensor, codes: torch.Tensor | None = None, rs: torch.Tensor | None = None):
@@ -240,7 +240,7 @@ class CudaLayer:
         if out is None and out_dtype is not None:
             out = torch.empty(M, self.o, dtype=out_dtype, device=codes.device)
         acc = torch.empty(M, self.o, dtype=torch.int32, device=codes.device) if want_acc else None
-        ws = workspace if workspace is not None else self.workspace(M)
+        ws = workspace  # None: the library's per-stream internal workspace
         od = OUT_F16 if (out is not None and out.dtype == torch.float16) else OUT_F32
         if out is not None:
             assert out.dtype in (torch.float16, torch.float32) and out.stride(1) == 1

@@ -14,6 +14,9 @@ OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libdgq_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# per-file extra flags: the grid search must not contract double mul+add into FMA
+# (bit-exact FP64 objectives against the reference, csrc/search.cu)
+EXTRA = {"search.cu": ["-fmad=false"]}
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
@@ -30,7 +33,7 @@ def _compile(src: str, verbose_ptxas: bool) -> tuple[str, str]:
         if os.path.isdir(os.path.join(ROOT, "include", "dgq")) else []
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(p) for p in [path] + deps):
         return obj, ""
-    cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *EXTRA.get(src, []), "-c", path, "-o", obj]
     if src.endswith(".cpp"):
         cmd[cmd.index("-c"):cmd.index("-c")] = ["-x", "cu"]
     if verbose_ptxas and src.endswith(".cu"):

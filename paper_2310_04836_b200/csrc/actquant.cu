@@ -46,64 +46,6 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
          ((static_cast<uint32_t>(c) & 0xFFu) << 16) | ((static_cast<uint32_t>(d) & 0xFFu) << 24);
 }
 
-// Vector path: K % 4 == 0, 16-B aligned rows, K <= 4*T*V.
-template <int T, int V>
-__global__ void __launch_bounds__(T) k_actquant_vec(const float* __restrict__ X, size_t ldx,
-                                                     const float* __restrict__ kv, int K, int Kpad,
-                                                     int dynamic, float act_scale, int8_t* __restrict__ Q,
-                                                     size_t ldq, float* __restrict__ rs, int M) {
-  __shared__ float red[33];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // let the GEMM start streaming weights
-  const int K4 = K >> 2;
-  for (int row = blockIdx.x; row < M; row += gridDim.x) {
-    const float4* xr = reinterpret_cast<const float4*>(X + static_cast<size_t>(row) * ldx);
-    const float4* k4 = reinterpret_cast<const float4*>(kv);
-    float4 xv[V];
-    float am = 0.0f;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int i = threadIdx.x + v * T;
-      if (i < K4) {
-        float4 x = __ldcs(xr + i);  // streamed once
-        float4 k = __ldg(k4 + i);
-        x.x = __fdiv_rn(x.x, k.x);
-        x.y = __fdiv_rn(x.y, k.y);
-        x.z = __fdiv_rn(x.z, k.z);
-        x.w = __fdiv_rn(x.w, k.w);
-        xv[v] = x;
-        am = fmaxf(am, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
-      }
-    }
-    float s = act_scale;
-    if (dynamic) s = dynamic_row_scale(block_max<T>(am, red));
-    if (threadIdx.x == 0) rs[row] = s;
-    uint32_t* qr = reinterpret_cast<uint32_t*>(Q + static_cast<size_t>(row) * ldq);
-    if (scale_is_safe(s)) {
-      const float inv = __frcp_rn(s);
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int i = threadIdx.x + v * T;
-        if (i < K4) {
-          const float4 x = xv[v];
-          qr[i] = pack4(quant_code_f32(x.x, s, inv), quant_code_f32(x.y, s, inv), quant_code_f32(x.z, s, inv),
-                        quant_code_f32(x.w, s, inv));
-        }
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int i = threadIdx.x + v * T;
-        if (i < K4) {
-          const float4 x = xv[v];
-          qr[i] = pack4(quant_code_f64(x.x, s), quant_code_f64(x.y, s), quant_code_f64(x.z, s),
-                        quant_code_f64(x.w, s));
-        }
-      }
-    }
-    for (int i = K4 + threadIdx.x; i < (Kpad >> 2); i += T) qr[i] = 0u;
-  }
-}
-
 // Generic path: any K / alignment.  Two passes over the row (the second hits L2).
 template <int T>
 __global__ void __launch_bounds__(T) k_actquant_any(const float* __restrict__ X, size_t ldx,
@@ -137,59 +79,7 @@ __global__ void __launch_bounds__(T) k_actquant_any(const float* __restrict__ X,
 //   X + (j / seg) * seg_stride + m * ldx + (j % seg)
 // so the next layer quantises the gathered [p][M][K/p] buffer in place.
 // float(x_f16) is exact, so this equals K1 on the float32 copy bit-for-bit.
-template <int T, int V>
-__global__ void __launch_bounds__(T) k_actquant_h8(const __half* __restrict__ X, size_t ldx, int seg, size_t seg_stride,
-                                                    const float* __restrict__ kv, int K, int Kpad, int dynamic,
-                                                    float act_scale, int8_t* __restrict__ Q, size_t ldq,
-                                                    float* __restrict__ rs, int M) {
-  __shared__ float red[33];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int K8 = K >> 3;
-  for (int row = blockIdx.x; row < M; row += gridDim.x) {
-    float xv[V][8];
-    float am = 0.0f;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int i = threadIdx.x + v * T;
-      if (i < K8) {
-        const int j = i * 8;
-        const __half* src = X + static_cast<size_t>(j / seg) * seg_stride + static_cast<size_t>(row) * ldx + (j % seg);
-        const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(src));
-        const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
-        const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
-        const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
-        const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float2 f = __half22float2(h2[t]);
-          xv[v][2 * t] = __fdiv_rn(f.x, kk[2 * t]);
-          xv[v][2 * t + 1] = __fdiv_rn(f.y, kk[2 * t + 1]);
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
-      }
-    }
-    float s = act_scale;
-    if (dynamic) s = dynamic_row_scale(block_max<T>(am, red));
-    if (threadIdx.x == 0) rs[row] = s;
-    uint2* qr = reinterpret_cast<uint2*>(Q + static_cast<size_t>(row) * ldq);
-    const bool safe = scale_is_safe(s);
-    const float inv = __frcp_rn(s);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int i = threadIdx.x + v * T;
-      if (i < K8) {
-        int c[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) c[t] = safe ? quant_code_f32(xv[v][t], s, inv) : quant_code_f64(xv[v][t], s);
-        qr[i] = make_uint2(pack4(c[0], c[1], c[2], c[3]), pack4(c[4], c[5], c[6], c[7]));
-      }
-    }
-    for (int i = K8 + threadIdx.x; i < (Kpad >> 3); i += T) qr[i] = make_uint2(0u, 0u);
-  }
-}
-
-// Generic FP16 path (any K / segment geometry).
+// Generic FP16 path (any K / segment geometry); the vector paths are k_actquant2/3.
 template <int T>
 __global__ void __launch_bounds__(T) k_actquant_h_any(const __half* __restrict__ X, size_t ldx, int seg,
                                                        size_t seg_stride, const float* __restrict__ kv, int K,
@@ -489,54 +379,6 @@ __global__ void k_div_check(const float* __restrict__ x, const float* __restrict
 
 using namespace dgqk;
 
-cudaError_t dgq_launch_actquant(const float* X, size_t ldx, const float* k, int K, int Kpad, int dynamic,
-                                float act_scale, int8_t* Q, size_t ldq, float* rs, int M, cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  const int grid = M;
-  const bool vec = (K % 4 == 0) && (ldx % 4 == 0) && (ldq % 4 == 0) && (Kpad % 4 == 0) &&
-                   (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(k) % 16 == 0) &&
-                   (reinterpret_cast<uintptr_t>(Q) % 4 == 0);
-  const int K4 = K / 4;
-  if (vec && K4 <= 256 * 1) {
-    k_actquant_vec<256, 1><<<grid, 256, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  } else if (vec && K4 <= 256 * 2) {
-    k_actquant_vec<256, 2><<<grid, 256, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  } else if (vec && K4 <= 256 * 4) {
-    k_actquant_vec<256, 4><<<grid, 256, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  } else if (vec && K4 <= 256 * 8) {
-    k_actquant_vec<256, 8><<<grid, 256, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  } else if (vec && K4 <= 512 * 8) {
-    k_actquant_vec<512, 8><<<grid, 512, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  } else if (vec && K4 <= 512 * 16) {
-    k_actquant_vec<512, 16><<<grid, 512, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  } else {
-    k_actquant_any<256><<<grid, 256, 0, st>>>(X, ldx, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-  }
-  return cudaGetLastError();
-}
-
-cudaError_t dgq_launch_actquant_f16(const void* Xv, size_t ldx, int seg, size_t seg_stride, const float* k, int K,
-                                    int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq, float* rs, int M,
-                                    cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  const __half* X = static_cast<const __half*>(Xv);
-  if (seg <= 0) seg = K;
-  const bool vec = (K % 8 == 0) && (seg % 8 == 0) && (ldx % 8 == 0) && (seg_stride % 8 == 0) && (ldq % 8 == 0) &&
-                   (Kpad % 8 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
-                   (reinterpret_cast<uintptr_t>(k) % 16 == 0) && (reinterpret_cast<uintptr_t>(Q) % 8 == 0);
-  const int K8 = K / 8;
-#define DGQ_H8(T_, V_) k_actquant_h8<T_, V_><<<M, T_, 0, st>>>(X, ldx, seg, seg_stride, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M)
-  if (vec && K8 <= 128) DGQ_H8(128, 1);
-  else if (vec && K8 <= 256) DGQ_H8(256, 1);
-  else if (vec && K8 <= 512) DGQ_H8(256, 2);
-  else if (vec && K8 <= 1024) DGQ_H8(256, 4);
-  else if (vec && K8 <= 2048) DGQ_H8(512, 4);
-  else if (vec && K8 <= 4096) DGQ_H8(512, 8);
-  else k_actquant_h_any<256><<<M, 256, 0, st>>>(X, ldx, seg, seg_stride, k, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);
-#undef DGQ_H8
-  return cudaGetLastError();
-}
-
 namespace {
 template <int T, int V, int CL, bool F16, bool CK>
 cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, const float* rk,
@@ -591,7 +433,7 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
   {                                                                                                             \
     auto kern = f16 ? (k_checked ? k_actquant3<T_, V_, true, false> : k_actquant3<T_, V_, true, true>)          \
                     : (k_checked ? k_actquant3<T_, V_, false, false> : k_actquant3<T_, V_, false, true>);       \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(stage));          \
+    { cudaError_t e_ = dgq_allow_smem(kern, stage); if (e_ != cudaSuccess) return e_; }                       \
     int occ = 1;                                                                                                \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, stage);                                       \
     const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \

@@ -11,12 +11,33 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/dgq_b200.h"
 #include "kernels.h"
 
 extern "C" int dgq_debug_decode_mode();
+
+cudaError_t dgq_allow_smem(const void* kernel, size_t bytes) {
+  // The limit only ever grows (to the largest size requested so far, per kernel
+  // and device), so a concurrent launch needing less can never shrink it under
+  // a launch needing more; it stays at what the calls need rather than the
+  // opt-in maximum, which keeps the driver's L1 / shared-memory carveout as
+  // large as the kernel allows.
+  static std::mutex mu;
+  static std::unordered_map<const void*, std::vector<size_t>> done;  // per device: limit set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  std::vector<size_t>& v = done[kernel];
+  if (v.size() <= static_cast<size_t>(dev)) v.resize(dev + 1, 0);
+  if (bytes <= v[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) v[dev] = bytes;
+  return e;
+}
 
 namespace {
 
@@ -129,10 +150,70 @@ struct dgq_layer {
   uint8_t* kone = nullptr;   // [h/8] chunk c's eight k are all exactly 1 (K1 skips their division)
   size_t device_bytes = 0;
   CUtensorMap tmA{};  // non-fused A operand
+  // Internal split-K workspaces for callers that pass none, one per stream:
+  // the stream-K partials and tile flags of a launch must not be shared with a
+  // launch on another stream (the kernels run after the host call returns).
+  // `ev` marks the last launch that used the slot, so a destroyed stream whose
+  // handle is reused while its work is pending cannot overlap it either.
+  struct StreamWs {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+  };
   std::mutex ws_mu;
-  void* ws = nullptr;
-  size_t ws_cap = 0;
+  std::unordered_map<cudaStream_t, StreamWs> ws;
 };
+
+// The layer's internal workspace for stream `st` (caller holds L->ws_mu),
+// grown to `need` zeroed bytes.  Outside stream capture the launch that uses it
+// is ordered after the previous user of the slot (ws_release records it).
+static dgq_status ws_acquire(dgq_layer* L, cudaStream_t st, size_t need, void** out, size_t* cap) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  DGQ_CUDA(cudaStreamIsCapturing(st, &cs));
+  auto& w = L->ws[st];
+  if (w.cap < need) {
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(DGQ_EINVAL, "internal workspace must grow during stream capture: call once before capturing or "
+                              "pass dWorkspace");
+    if (w.p) {
+      DGQ_CUDA(cudaEventSynchronize(w.ev));
+      cudaFree(w.p);
+      w.p = nullptr;
+      w.cap = 0;
+    }
+    DGQ_CUDA(cudaMalloc(&w.p, need));
+    DGQ_CUDA(cudaMemsetAsync(w.p, 0, need, st));
+    w.cap = need;
+  }
+  if (!w.ev) DGQ_CUDA(cudaEventCreateWithFlags(&w.ev, cudaEventDisableTiming));
+  if (w.used && cs == cudaStreamCaptureStatusNone) DGQ_CUDA(cudaStreamWaitEvent(st, w.ev, 0));
+  *out = w.p;
+  *cap = w.cap;
+  return DGQ_OK;
+}
+
+// Argument checks shared by dgq_linear and every layer of dgq_linear_multi
+// (the reference's preconditions of int8_gemm, proj/src/kernel.cpp:47-54).
+static dgq_status check_linear_args(const dgq_layer* L, const int8_t* dXq, size_t ldq, const float* dRs, size_t M,
+                                    const void* dY, size_t ldy, const int32_t* dAcc, size_t ld_acc) {
+  if (!dXq || !dRs) return fail(DGQ_EINVAL, "null activation codes or row scales");
+  if (ldq != L->k_pad) return fail(DGQ_EINVAL, "ldq must equal the layer's k_pad (" + std::to_string(L->k_pad) + ")");
+  if (reinterpret_cast<uintptr_t>(dXq) % 16) return fail(DGQ_EINVAL, "activation codes must be 16-byte aligned");
+  if (dY && ldy < L->o) return fail(DGQ_EINVAL, "ldy smaller than the output width");
+  if (dAcc && ld_acc < L->o) return fail(DGQ_EINVAL, "ld_acc smaller than the output width");
+  if (M > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too many rows");
+  if (static_cast<double>(L->h) * 127.0 * 127.0 >= 2147483648.0)
+    return fail(DGQ_EINVAL, "h too large for 32-bit accumulation");
+  return DGQ_OK;
+}
+
+static void ws_release(dgq_layer* L, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  auto& w = L->ws[st];
+  if (cudaEventRecord(w.ev, st) == cudaSuccess) w.used = true;
+}
 
 extern "C" {
 
@@ -247,7 +328,10 @@ void dgq_layer_destroy(dgq_layer* L) {
   cudaFree(L->k);
   cudaFree(L->rk);
   cudaFree(L->kone);
-  cudaFree(L->ws);
+  for (auto& kv : L->ws) {
+    cudaFree(kv.second.p);
+    if (kv.second.ev) cudaEventDestroy(kv.second.ev);
+  }
   cudaSetDevice(prev);
   delete L;
 }
@@ -268,7 +352,13 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
   if (col_begin >= col_end || col_end > o) return fail(DGQ_EINVAL, "bad column shard range");
   if (h > (1u << 30) || o > (1u << 30)) return fail(DGQ_EINVAL, "layer too large");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int prev_dev = 0;
+  DGQ_CUDA(cudaGetDevice(&prev_dev));
   DGQ_CUDA(cudaSetDevice(device));
+  struct RestoreDevice {
+    int d;
+    ~RestoreDevice() { cudaSetDevice(d); }
+  } restore_dev{prev_dev};
 
   auto* L = new dgq_layer();
   L->device = device;
@@ -642,30 +732,21 @@ dgq_status dgq_linear(const dgq_layer* Lc, const int8_t* dXq, size_t ldq, const 
   auto* L = const_cast<dgq_layer*>(Lc);
   if (!L) return fail(DGQ_EINVAL, "null layer");
   if (M == 0) return DGQ_OK;
-  if (!dXq || !dRs) return fail(DGQ_EINVAL, "null activation codes or row scales");
-  if (ldq != L->k_pad) return fail(DGQ_EINVAL, "ldq must equal the layer's k_pad (" + std::to_string(L->k_pad) + ")");
-  if (reinterpret_cast<uintptr_t>(dXq) % 16) return fail(DGQ_EINVAL, "activation codes must be 16-byte aligned");
-  if (dY && ldy < L->o) return fail(DGQ_EINVAL, "ldy smaller than the output width");
-  if (dAcc && ld_acc < L->o) return fail(DGQ_EINVAL, "ld_acc smaller than the output width");
-  if (M > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too many rows");
-  if (static_cast<double>(L->h) * 127.0 * 127.0 >= 2147483648.0)
-    return fail(DGQ_EINVAL, "h too large for 32-bit accumulation");
+  {
+    dgq_status s = check_linear_args(L, dXq, ldq, dRs, M, dY, ldy, dAcc, ld_acc);
+    if (s != DGQ_OK) return s;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t need = dgq_linear_workspace_bytes(L, M);
   void* ws = dWorkspace;
-  std::unique_lock<std::mutex> lk(L->ws_mu, std::defer_lock);
   if (need && !ws) {
-    lk.lock();
-    if (L->ws_cap < need) {
-      cudaFree(L->ws);
-      L->ws = nullptr;
-      L->ws_cap = 0;
-      DGQ_CUDA(cudaMalloc(&L->ws, need));
-      DGQ_CUDA(cudaMemset(L->ws, 0, need));
-      L->ws_cap = need;
-    }
-    ws = L->ws;
-    ws_bytes = L->ws_cap;
+    std::lock_guard<std::mutex> lk(L->ws_mu);
+    dgq_status s = ws_acquire(L, st, need, &ws, &ws_bytes);
+    if (s != DGQ_OK) return s;
+    s = run_gemm(L->fused, L->tiles, L->tmA, static_cast<int>(L->g), L->o, L->k_pad, dXq, ldq, M, dRs, L->s1, dBias,
+                 out_dtype, fp16_mode, dY, ldy, dAcc, ld_acc, ws, ws_bytes, st);
+    ws_release(L, st);
+    return s;
   }
   return run_gemm(L->fused, L->tiles, L->tmA, static_cast<int>(L->g), L->o, L->k_pad, dXq, ldq, M, dRs, L->s1,
                   dBias, out_dtype, fp16_mode, dY, ldy, dAcc, ld_acc, ws, ws_bytes, st);
@@ -775,7 +856,6 @@ dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW
   if (!max_abs_acc) return fail(DGQ_EINVAL, "null output");
   *max_abs_acc = 0;
   if (M == 0 || N == 0 || K == 0) return DGQ_OK;
-  if (M > 65535) return fail(DGQ_EINVAL, "audit supports at most 65535 rows");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* d = nullptr;
   DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), st));
@@ -857,8 +937,13 @@ dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int
     if (!layers[i] || !dY[i]) return fail(DGQ_EINVAL, "null layer or output");
     if (layers[i]->h != L0->h || layers[i]->g != L0->g || layers[i]->fused != L0->fused)
       return fail(DGQ_EINVAL, "dgq_linear_multi: layers must share h, g and the prepared layout");
+    if (layers[i]->device != L0->device) return fail(DGQ_EINVAL, "dgq_linear_multi: layers on different devices");
   }
   if (M == 0) return DGQ_OK;
+  for (int i = 0; i < count; ++i) {
+    dgq_status s = check_linear_args(layers[i], dXq, ldq, dRowScale, M, dY[i], ldy[i], nullptr, 0);
+    if (s != DGQ_OK) return s;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int total_tiles = 0;
   for (int i = 0; i < count; ++i) total_tiles += layers[i]->n_tiles;
@@ -872,30 +957,24 @@ dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int
     }
     return DGQ_OK;
   }
-  if (ldq != L0->k_pad) return fail(DGQ_EINVAL, "ldq must equal the layers' k_pad");
-  if (!dXq || !dRowScale) return fail(DGQ_EINVAL, "null activation codes or row scales");
   const size_t need = pl.ws_bytes + pl.counter_bytes;
   void* ws = dWorkspace;
-  auto* L = const_cast<dgq_layer*>(L0);
-  std::unique_lock<std::mutex> lk(L->ws_mu, std::defer_lock);
-  if (!ws) {  // the first layer's internal workspace, grown to the combined problem
-    lk.lock();
-    if (L->ws_cap < need) {
-      cudaFree(L->ws);
-      L->ws = nullptr;
-      L->ws_cap = 0;
-      DGQ_CUDA(cudaMalloc(&L->ws, need));
-      DGQ_CUDA(cudaMemset(L->ws, 0, need));
-      L->ws_cap = need;
-    }
-    ws = L->ws;
-  } else if (ws_bytes < need) {
-    return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(need));
-  }
   DecodeSub subs[kDecodeMaxSub];
   for (int i = 0; i < count; ++i)
     subs[i] = DecodeSub{layers[i]->tiles, layers[i]->s1, dBias ? dBias[i] : nullptr, dY[i], ldy[i],
                         static_cast<int>(layers[i]->o)};
+  if (!ws) {  // the first layer's internal workspace for this stream, grown to the combined problem
+    auto* L = const_cast<dgq_layer*>(L0);
+    std::lock_guard<std::mutex> lk(L->ws_mu);
+    size_t cap = 0;
+    dgq_status s = ws_acquire(L, st, need, &ws, &cap);
+    if (s != DGQ_OK) return s;
+    s = run_decode(subs, count, static_cast<int>(L0->g), L0->k_pad, dXq, ldq, M, dRowScale, out_dtype, 0, nullptr, 0,
+                   ws, st);
+    ws_release(L, st);
+    return s;
+  }
+  if (ws_bytes < need) return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(need));
   return run_decode(subs, count, static_cast<int>(L0->g), L0->k_pad, dXq, ldq, M, dRowScale, out_dtype, 0, nullptr, 0,
                     ws, st);
 }
@@ -907,6 +986,83 @@ size_t dgq_linear_multi_workspace_bytes(const dgq_layer* const* layers, int coun
   DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), total_tiles * 128, static_cast<int>(layers[0]->k_pad),
                                  layers[0]->fused, static_cast<int>(layers[0]->g));
   return pl.ws_bytes + pl.counter_bytes;
+}
+
+// ---- offline quantiser: two-phase grid search -------------
+static dgq_status upload_grid(const float* grid, size_t n, float** d, cudaStream_t st) {
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(d), n * sizeof(float), st));
+  DGQ_CUDA(cudaMemcpyAsync(*d, grid, n * sizeof(float), cudaMemcpyHostToDevice, st));
+  return DGQ_OK;
+}
+
+dgq_status dgq_phase1_search(const float* dW, size_t h, size_t o, const float* dX, const float* dXhat, size_t b,
+                             size_t g, int n_bits, const float* alpha_grid, size_t n_alpha, float* dSprime,
+                             int32_t* dZp, float* dErr, float* dAlpha, uint64_t* evals, void* stream) {
+  // SearchConfig::validate (proj/src/search.cpp:24-45)
+  if (g < 1 || h % g != 0)
+    return fail(DGQ_EINVAL, "group size " + std::to_string(g) + " must divide h = " + std::to_string(h));
+  if (n_bits < 2 || n_bits > 8) return fail(DGQ_EINVAL, "n_bits_w must be in [2, 8]");
+  if (!alpha_grid || n_alpha == 0) return fail(DGQ_EINVAL, "alpha_grid_phase1 is empty");
+  for (size_t i = 0; i < n_alpha; ++i)
+    if (!(alpha_grid[i] > 0.0f && alpha_grid[i] <= 1.0f))
+      return fail(DGQ_EINVAL, "alpha_grid_phase1 values must be in (0, 1]");
+  if (evals) *evals = static_cast<uint64_t>(h / g) * o * n_alpha;
+  if (o == 0 || h == 0) return DGQ_OK;
+  if (!dW || (b && (!dX || !dXhat)) || !dSprime || !dZp || !dErr || !dAlpha) return fail(DGQ_EINVAL, "null argument");
+  const size_t n_g = h / g;
+  if (h > 0x7FFFFFFF || o * n_alpha > 0x7FFFFFFF || b > 0x7FFFFFFF || n_g > 65535)
+    return fail(DGQ_EINVAL, "search problem too large");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float *da = nullptr, *mn = nullptr, *mx = nullptr;
+  double *ref = nullptr, *err = nullptr;
+  dgq_status s = upload_grid(alpha_grid, n_alpha, &da, st);
+  if (s != DGQ_OK) return s;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mn), n_g * o * sizeof(float), st));
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&mx), n_g * o * sizeof(float), st));
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ref), (n_g * o * b + 1) * sizeof(double), st));
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&err), n_g * o * n_alpha * sizeof(double), st));
+  cudaError_t e = dgq_launch_phase1(dW, dX, dXhat, static_cast<int>(h), static_cast<int>(o), static_cast<int>(b),
+                                    static_cast<int>(g), (1 << n_bits) - 1, da, static_cast<int>(n_alpha), mn, mx,
+                                    ref, err, dSprime, dZp, dErr, dAlpha, st);
+  cudaFreeAsync(da, st);
+  cudaFreeAsync(mn, st);
+  cudaFreeAsync(mx, st);
+  cudaFreeAsync(ref, st);
+  cudaFreeAsync(err, st);
+  DGQ_CUDA(e);
+  return DGQ_OK;
+}
+
+dgq_status dgq_phase2_search(const float* dW, size_t h, size_t o, const float* dX, const float* dXhat, size_t b,
+                             size_t g, const float* dSprime, const int32_t* dZp, const float* alpha_grid,
+                             size_t n_alpha, float* dS1, int8_t* dS2, int32_t* dCodes, double* dColErr,
+                             float* dColAlpha, uint64_t* evals, void* stream) {
+  if (g == 0 || h % g != 0) return fail(DGQ_EINVAL, "GroupParams shape does not match weights");
+  if (!alpha_grid || n_alpha == 0) return fail(DGQ_EINVAL, "alpha_grid_phase2 is empty");
+  if (evals) *evals = static_cast<uint64_t>(o) * n_alpha;
+  if (o == 0 || h == 0) return DGQ_OK;
+  if (!dW || (b && (!dX || !dXhat)) || !dSprime || !dZp || !dS1 || !dS2 || !dCodes || !dColErr || !dColAlpha)
+    return fail(DGQ_EINVAL, "null argument");
+  const size_t n_g = h / g;
+  if (h > 0x7FFFFFFF || o * n_alpha > 0x7FFFFFFF || b > 0x7FFFFFFF || n_g > 65535)
+    return fail(DGQ_EINVAL, "search problem too large");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float *da = nullptr, *am = nullptr;
+  double *ref = nullptr, *err = nullptr;
+  dgq_status s = upload_grid(alpha_grid, n_alpha, &da, st);
+  if (s != DGQ_OK) return s;
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&am), o * sizeof(float), st));
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ref), (o * b + 1) * sizeof(double), st));
+  DGQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&err), o * n_alpha * sizeof(double), st));
+  cudaError_t e = dgq_launch_phase2(dW, dX, dXhat, static_cast<int>(h), static_cast<int>(o), static_cast<int>(b),
+                                    static_cast<int>(g), dSprime, dZp, da, static_cast<int>(n_alpha), am, ref, err,
+                                    dS1, dS2, dCodes, dColErr, dColAlpha, st);
+  cudaFreeAsync(da, st);
+  cudaFreeAsync(am, st);
+  cudaFreeAsync(ref, st);
+  cudaFreeAsync(err, st);
+  DGQ_CUDA(e);
+  return DGQ_OK;
 }
 
 }  // extern "C"

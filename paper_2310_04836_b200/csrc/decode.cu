@@ -472,7 +472,7 @@ static cudaError_t launch_dec(const CUtensorMap& tmB, const DgqDecodeParams& p, 
                               cudaStream_t st) {
   auto kern = k_dgq_decode<BN, SL, UPS>;
   const size_t smem = dgq_decode_smem_bytes(BN, SL * UPS, p.chunk_bytes);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);

@@ -30,9 +30,9 @@ __global__ void k_epilogue(const int32_t* __restrict__ acc, size_t lda, const fl
 __global__ void k_audit(const int8_t* __restrict__ Xq, size_t ldx, const int8_t* __restrict__ W, size_t ldw, int M,
                         int K, int N, unsigned long long* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
   int32_t best = 0;
-  if (c < N && r < M) {
+  for (int r = blockIdx.y; r < M; r += gridDim.y) {  // any M: rows beyond grid.y loop
+    if (c >= N) break;
     const int8_t* x = Xq + static_cast<size_t>(r) * ldx;
     int32_t s = 0;
     for (int i = 0; i < K; ++i) {
@@ -61,7 +61,7 @@ cudaError_t dgq_launch_epilogue(const int32_t* acc, size_t lda, const float* rs,
 cudaError_t dgq_launch_audit(const int8_t* Xq, size_t ldx, const int8_t* W, size_t ldw, int M, int K, int N,
                              unsigned long long* out, cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  dim3 grid((N + 127) / 128, M);
+  dim3 grid((N + 127) / 128, M < 65535 ? M : 65535);
   k_audit<<<grid, 128, 0, st>>>(Xq, ldx, W, ldw, M, K, N, out);
   return cudaGetLastError();
 }

@@ -493,7 +493,7 @@ cudaError_t launch_one(const DgqGemmPlan& plan, const CUtensorMap& tmB, const CU
   using C = Cfg<BN, NT, SL, SA, DQW, kFused>;
   auto kern = k_dgq_gemm<BN, NT, SL, SA, DQW, kFused>;
   const size_t smem = C::smem_bytes(p.chunk_stride);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(plan.m_tiles, (plan.n_tiles + NT - 1) / NT, plan.splits);
@@ -556,7 +556,10 @@ double est_cycles(int M, int N, int kblocks, int bn, int nt, int splits, bool fu
 }  // namespace
 
 namespace {
-int g_decode_mode = 1;  // tools: 0 = never use K5d (A/B comparisons against the prefill orientation)
+// Test/tools override of the planner (0 = never use K5d; other bits force work
+// splits).  Thread-local: an override set by one host thread never changes the
+// plans of another caller of the library.
+thread_local int g_decode_mode = 1;
 int sm_count() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -566,7 +569,7 @@ int sm_count() {
 
 extern "C" void dgq_debug_set_decode(int mode) { g_decode_mode = mode; }
 namespace {
-int g_pair_cap = 0;
+thread_local int g_pair_cap = 0;
 }
 extern "C" void dgq_debug_set_pair_cap(int cap) { g_pair_cap = cap; }
 int dgq_prefill2_cluster_cap() { return g_pair_cap; }

@@ -139,9 +139,6 @@ cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, 
 cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorMap& tmB, const CUtensorMap& tmA,
                             const CUtensorMap& tmY, const DgqGemmParams& p, cudaStream_t st);
 
-cudaError_t dgq_launch_actquant(const float* X, size_t ldx, const float* k, int K, int Kpad, int dynamic,
-                                float act_scale, int8_t* Q, size_t ldq, float* rs, int M, cudaStream_t st);
-
 // K1 v2 (f32 or f16 input; f16 may be the all-gathered [p][M][seg] layout);
 // rk = RN(1/k) per input channel (dgq_launch_reciprocal).
 cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, size_t seg_stride, const float* k,
@@ -151,10 +148,27 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
 cudaError_t dgq_launch_reciprocal(const float* k, float* rk, int n, cudaStream_t st);
 cudaError_t dgq_launch_div_check(const float* x, const float* k, float* fast, float* ieee, int n, cudaStream_t st);
 
-// FP16 activations, optionally the all-gathered [p][M][seg] layout (seg = K/p).
-cudaError_t dgq_launch_actquant_f16(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, int K,
-                                    int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq, float* rs, int M,
-                                    cudaStream_t st);
+// Two-phase grid search (csrc/search.cu).  Scratch: mn/mx [n_g x o] floats,
+// ref [n_g x o x b] doubles, err [n_g x o x n_alpha] doubles (phase 1);
+// absmax [o] floats, ref [o x b], err [o x n_alpha] doubles (phase 2).
+cudaError_t dgq_launch_phase1(const float* W, const float* X, const float* Xhat, int h, int o, int b, int g,
+                              int levels, const float* alpha, int n_alpha, float* mn, float* mx, double* ref,
+                              double* err, float* sp, int32_t* zp, float* err_out, float* alpha_out,
+                              cudaStream_t st);
+cudaError_t dgq_launch_phase2(const float* W, const float* X, const float* Xhat, int h, int o, int b, int g,
+                              const float* sp, const int32_t* zp, const float* alpha, int n_alpha, float* absmax,
+                              double* ref, double* err, float* s1, int8_t* s2, int32_t* codes, double* col_err,
+                              float* col_alpha, cudaStream_t st);
+
+// Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum,
+// once per (kernel, device) under a lock, so concurrent launches of one
+// instantiation with different sizes never shrink each other's limit.
+// cudaErrorInvalidValue when `bytes` exceeds the opt-in maximum.
+cudaError_t dgq_allow_smem(const void* kernel, size_t bytes);
+template <typename F>
+inline cudaError_t dgq_allow_smem(F* kernel, size_t bytes) {
+  return dgq_allow_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
 
 // Reference layout (codes u4 [h x o_full] packed along o, s2 i8, zp u4) column
 // slice [c0, c0+n) -> prepared tiles.

@@ -982,7 +982,7 @@ static int max_active_pairs() {
   int n = sms / 2;
   const size_t smem = smem_bytes_s<S>(static_cast<uint32_t>(dgq_layout::chunk_bytes(128)));
   auto kern = k_dgq_prefill2<TN, S>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) ==
+  if (dgq_allow_smem(kern, smem) ==
       cudaSuccess) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * n);
@@ -1024,7 +1024,7 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
                              cudaStream_t st) {
   const size_t smem = smem_bytes_s<S>(p.chunk_stride);
   auto kern = k_dgq_prefill2<TN, S>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN, p.k_blocks, p.stream_k != 0, S));

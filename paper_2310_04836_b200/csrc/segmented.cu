@@ -64,7 +64,7 @@ cudaError_t dgq_launch_segmented(const int8_t* Xq, size_t ldx, const float* rs, 
                                  float* y, size_t ldy, cudaStream_t st) {
   if (M <= 0 || o <= 0) return cudaSuccess;
   if (h > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_segmented, cudaFuncAttributeMaxDynamicSharedMemorySize, h);
+    cudaError_t e = dgq_allow_smem(k_segmented, static_cast<size_t>(h));
     if (e != cudaSuccess) return e;
   }
   dim3 grid((o + 127) / 128, M);

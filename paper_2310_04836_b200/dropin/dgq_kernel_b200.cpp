@@ -30,6 +30,16 @@
 namespace dgq {
 namespace {
 
+// DGQ_EFORMAT carries the reference's format_error::kind name in the error field
+// (proj/include/dgq/error.hpp:18-24).
+format_error::kind format_kind(const std::string& f) {
+  if (f == "bad_magic") return format_error::kind::bad_magic;
+  if (f == "truncated") return format_error::kind::truncated;
+  if (f == "size_mismatch") return format_error::kind::size_mismatch;
+  if (f == "unknown_dtype") return format_error::kind::unknown_dtype;
+  return format_error::kind::bad_header;
+}
+
 void check(dgq_status st) {
   if (st == DGQ_OK) return;
   const std::string msg = dgq_last_error();
@@ -39,7 +49,7 @@ void check(dgq_status st) {
     case DGQ_EVALIDATION:
       throw validation_error(dgq_last_error_field(), msg);
     case DGQ_EFORMAT:
-      throw format_error(format_error::kind::bad_header, msg);
+      throw format_error(format_kind(dgq_last_error_field()), msg);
     default:
       throw std::runtime_error("dgq_b200: " + msg);
   }

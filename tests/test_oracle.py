@@ -178,3 +178,21 @@ def test_bench_smoothing_vector_is_the_references(port, ref, h):
     assert np.array_equal(synth.smooth_k(h).view(np.uint32), k_ref.view(np.uint32))
     if h == 7168:  # the K1 unit-k fast path covers most chunks
         assert (k_ref.reshape(-1, 8) == 1.0).all(axis=1).mean() > 0.9
+
+
+def test_vectorised_fp16_round_equals_reference(port, golden):
+    # oracle.fp16_round_np (used by the full-size GPU parity tests and bench.py's
+    # self-check) against the scalar restatement on the golden points, every
+    # exponent x a spread of mantissas (incl. the (2^-25, 2^-24) flush band) and
+    # random finite values
+    import oracle
+
+    x = golden["fp16.x"]
+    assert np.array_equal(oracle.fp16_round_np(x).view(np.uint32), golden["fp16.y"].view(np.uint32))
+    bits = np.array([(s << 31) | (e << 23) | m for s in (0, 1) for e in range(0, 255)
+                     for m in (0, 1, 0xFFF, 0x1000, 0x1001, 0x1FFF, 0x2000, 0x3000, 0x7FFFFF, 0x400000)], np.uint32)
+    rnd = np.random.default_rng(5).integers(0, 0x7F800000, 20000, dtype=np.uint32)
+    rnd |= (np.arange(rnd.size, dtype=np.uint32) & 1) << 31
+    for b in (bits, rnd):
+        x = b.view(np.float32)
+        assert np.array_equal(oracle.fp16_round_np(x).view(np.uint32), port.fp16_round_array(x).view(np.uint32))

@@ -630,3 +630,29 @@ def test_prefill_fp16_flush_range(cuda, port, s1_scale):
     assert np.array_equal(y16.cpu().numpy().view(np.uint16), ref.view(np.uint16))
     if s1_scale < 1e-6:
         assert (np.abs(out) < 2.0 ** -24).any() and (out != 0).any()
+
+
+@pytest.mark.parametrize("M,o", [(8, 1024), (512, 4096)])
+def test_shared_layer_concurrent_streams_internal_workspace(cuda, port, decode_kernel, M, o):
+    # One prepared layer used from two streams at once with no caller workspace:
+    # each stream gets its own internal split-K workspace (stream-K partials and
+    # tile flags), so concurrent K5d (M = 8) / K5p (M = 512) launches cannot fold
+    # in each other's partials; every result equals the oracle bit for bit.
+    h = 7168
+    L = oracle.random_layer(h, o, 128, seed=o + M)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    assert dgq.lib().dgq_linear_workspace_bytes(CL.handle, M) > 0  # the call splits tiles
+    Xs = [port.gen_synthetic(M, h, 40 + i, 3, 50.0, 3) for i in range(2)]
+    refs = [port.dgq_forward(X, L)[0] for X in Xs]
+    ins = [CL.quantize_act(torch.from_numpy(X).cuda()) for X in Xs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    for _ in range(12):
+        for i, s in enumerate(streams):
+            with torch.cuda.stream(s):
+                outs[i].append(CL.linear(*ins[i], out_dtype=torch.float32))
+    torch.cuda.synchronize()
+    for i in range(2):
+        for y in outs[i]:
+            assert np.array_equal(bits(y.cpu().numpy()), bits(refs[i]))
