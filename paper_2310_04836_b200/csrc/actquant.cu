@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 #include <cuda_fp16.h>
@@ -110,57 +111,64 @@ __global__ void __launch_bounds__(T) k_actquant_h_any(const __half* __restrict__
   }
 }
 
-// ---- K1 v2: one row per CL-CTA cluster, 8-element chunks, loads front-loaded ----
-// chunk c of a row (elements 8c..8c+7) belongs to cluster rank c / (T*V); every
-// thread first issues all of its V 16-B (f16) or 32-B (f32) loads, then divides
-// by k with the hoisted reciprocal (div_k), reduces the row absmax (block, then
-// over the cluster through DSMEM), and quantises from registers.
-// x' = x / k for one 8-channel chunk c.  kone[c] != 0 marks a chunk whose eight
-// k are exactly 1 (compute_smooth, proj/src/smoothing.cpp:45-47, gives k =
-// max(1, z/threshold): all but the top `percentile` channels): x / 1 == x in
-// IEEE arithmetic for every finite x, so the division and the k / RN(1/k)
-// loads are skipped.
-template <bool kCheckX, bool kCheckK>
-__device__ __forceinline__ void smooth_chunk(const float (&x)[8], const float* __restrict__ kv,
-                                             const float* __restrict__ rkv, bool unit, int c, float (&q)[8]) {
-  if (unit) {
-#pragma unroll
-    for (int t = 0; t < 8; ++t) q[t] = x[t];
-    return;
-  }
-  const int j = c * 8;
-  const float4 k0 = __ldg(reinterpret_cast<const float4*>(kv + j));
-  const float4 k1 = __ldg(reinterpret_cast<const float4*>(kv + j + 4));
-  const float4 r0 = __ldg(reinterpret_cast<const float4*>(rkv + j));
-  const float4 r1 = __ldg(reinterpret_cast<const float4*>(rkv + j + 4));
-  const float kk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-  const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-  div_chunk<kCheckX, kCheckK>(x, kk, rr, q);
-}
+// ---- vector paths (K % 8 == 0, 16-byte aligned rows) -------------------------
+// Elements are handled in 8-channel chunks.  ksm[c] (built once per layer) has
+// bit t set when k[8c + t] != 1: only those channels divide (smooth_sparse).
+// Chunk c of a row belongs to thread (c mod T) (plus the cluster rank for v2),
+// so every warp load or store instruction touches contiguous memory.
 
-// Bit v: chunk threadIdx.x-based index cbase + v*T is a unit-k chunk.  Built
-// once per kernel with all V flag loads in flight together (a flag load per
-// chunk inside the row loop was a dependent L2 round trip: 34 % of K1's stall
-// samples, profiles/ncu_summary_r01c.json era capture).
+// Bits 8v..8v+7: the k != 1 mask of the thread's v-th chunk (V <= 4).  Built
+// once per kernel with all V loads in flight together.
 template <int T, int V>
-__device__ __forceinline__ uint32_t unit_mask(const uint8_t* __restrict__ kone, int cbase, int C8) {
-  if (!kone) return 0u;
-  uint8_t f[V];
+__device__ __forceinline__ uint32_t special_masks(const uint8_t* __restrict__ ksm, int cbase, int C8) {
+  static_assert(V <= 4, "one byte per chunk in a 32-bit word");
+  if (!ksm) return 0xFFFFFFFFu;  // no layer mask: every channel divides
+  uint32_t m = 0;
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int c = cbase + v * T;
-    f[v] = c < C8 ? __ldg(kone + c) : 0;
+    if (c < C8) m |= static_cast<uint32_t>(__ldg(ksm + c)) << (8 * v);
   }
-  uint32_t m = 0;
-#pragma unroll
-  for (int v = 0; v < V; ++v) m |= (f[v] ? 1u : 0u) << v;
   return m;
 }
 
-template <int T, int V, int CL, bool kF16, bool kCheckK>
+// 8 input values of chunk c from a row in registers / shared memory as FP32
+template <bool kF16>
+__device__ __forceinline__ void unpack8(const uint4* raw, float (&x)[8]) {
+  if constexpr (kF16) {
+    const __half2* h2 = reinterpret_cast<const __half2*>(raw);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 f = __half22float2(h2[t]);
+      x[2 * t] = f.x;
+      x[2 * t + 1] = f.y;
+    }
+  } else {
+    const float* f = reinterpret_cast<const float*>(raw);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x[t] = f[t];
+  }
+}
+
+// codes of one chunk: the fast exact path for normal scales, doubles otherwise
+static __device__ __noinline__ uint2 chunk_codes_f64(float4 a, float4 b, float s) {
+  return make_uint2(pack4(quant_code_f64(a.x, s), quant_code_f64(a.y, s), quant_code_f64(a.z, s), quant_code_f64(a.w, s)),
+                    pack4(quant_code_f64(b.x, s), quant_code_f64(b.y, s), quant_code_f64(b.z, s), quant_code_f64(b.w, s)));
+}
+template <bool kStatic>
+__device__ __forceinline__ uint2 chunk_codes(const float (&xp)[8], float s, float inv, bool safe) {
+  if (safe) return quant_chunk<kStatic>(xp, s, inv);
+  return chunk_codes_f64(make_float4(xp[0], xp[1], xp[2], xp[3]), make_float4(xp[4], xp[5], xp[6], xp[7]), s);
+}
+
+// ---- K1 v2 (small M): one row per CL-CTA cluster, loads front-loaded ---------
+// every thread first issues all of its V 16-B (f16) or 32-B (f32) loads, then
+// smooths, reduces the row absmax (block, then over the cluster through DSMEM)
+// and quantises from registers.
+template <int T, int V, int CL, bool kF16, bool kDyn>
 __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
                                                   const float* __restrict__ kv, const float* __restrict__ rkv,
-                                                  const uint8_t* __restrict__ kone, int K, int Kpad, int dynamic,
+                                                  const uint8_t* __restrict__ ksm, int K, int Kpad,
                                                   float act_scale, int8_t* __restrict__ Q, size_t ldq,
                                                   float* __restrict__ rs, int M) {
   __shared__ float red[33];
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
   if (row >= M) return;  // grid is exactly M*CL; keeps the cluster barrier uniform
   const int C8 = K >> 3;
   const int cbase = part * T * V + threadIdx.x;
-  const uint32_t umask = unit_mask<T, V>(kone, cbase, C8);
+  const uint32_t sm = special_masks<T, V>(ksm, cbase, C8);
   uint4 raw[V][kF16 ? 1 : 2];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -195,28 +203,14 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
   for (int v = 0; v < V; ++v) {
     const int c = cbase + v * T;
     if (c < C8) {
-      const int j = c * 8;
-      float x[8];
-      if constexpr (kF16) {
-        const __half2* h2 = reinterpret_cast<const __half2*>(&raw[v][0]);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float2 f = __half22float2(h2[t]);
-          x[2 * t] = f.x;
-          x[2 * t + 1] = f.y;
-        }
-      } else {
-        const float* f = reinterpret_cast<const float*>(&raw[v][0]);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) x[t] = f[t];
-      }
-      smooth_chunk<!kF16, kCheckK>(x, kv, rkv, (umask >> v) & 1u, c, xv[v]);
+      unpack8<kF16>(raw[v], xv[v]);
+      smooth_sparse(xv[v], (sm >> (8 * v)) & 0xFFu, kv, rkv, c * 8);
 #pragma unroll
       for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
     }
   }
   float s = act_scale;
-  if (dynamic) {
+  if constexpr (kDyn) {
     float bm = block_max<T>(am, red);
     if constexpr (CL > 1) {
       cg::cluster_group cluster = cg::this_cluster();
@@ -235,39 +229,49 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int c = cbase + v * T;
-    if (c < C8) {
-      int o[8];
-      if (safe) {
-        if (dynamic)
-          quant_chunk<false>(xv[v], s, inv, o);
-        else
-          quant_chunk<true>(xv[v], s, inv, o);
-      } else {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) o[t] = quant_code_f64(xv[v][t], s);
-      }
-      qr[c] = make_uint2(pack4(o[0], o[1], o[2], o[3]), pack4(o[4], o[5], o[6], o[7]));
-    }
+    if (c < C8) qr[c] = chunk_codes<!kDyn>(xv[v], s, inv, safe);
   }
   if (part == 0)
     for (int c = C8 + threadIdx.x; c < (Kpad >> 3); c += T) qr[c] = make_uint2(0u, 0u);
 }
 
 // ---- K1 v3 (large M): persistent CTAs, whole rows staged in shared memory by
-// 1-D TMA bulk copies two rows ahead (double buffer, one mbarrier each), so
-// the HBM stream never waits for the divide / reduce / quantise of the
-// previous row.  x' = x/k stays in registers between the absmax and the codes.
-template <int T, int V, bool kF16, bool kCheckK>
+// 1-D TMA bulk copies through a ring of `depth` row buffers (one mbarrier
+// each).  Both passes read the row from shared memory (nothing row-sized is
+// held in registers), so a CTA of T threads covers a row in V = K / (8 T)
+// chunks per thread and the per-row fixed costs (the waits, two barriers, the
+// reduction) are spread over many chunks.
+//
+// Per row:
+//   1. the channels with k != 1 (compute_smooth leaves k == 1 on all but the
+//      top percentile; at most T of them — kSparse) are owned by threads of
+//      their own: thread i < nspec reads x[spec[i]], forms x' = x / k with k
+//      and RN(1/k) in registers, and overwrites the staged value with 0;
+//   2. barrier; absmax over the row (FP16 rows in packed form: |x| of a
+//      binary16 value orders like its magnitude bits, so an unsigned 16-bit max
+//      of the sign-cleared halves is the exact maximum; no conversion), the
+//      specials' |x'| folded in, warp maxima to a per-parity slot;
+//   3. barrier; every warp reduces the slots itself; the buffer of the
+//      PREVIOUS row (its second pass retired before this barrier) is refilled;
+//   4. codes from the staged row (a special's lane reads 0 -> code 0); the
+//      special thread's own code byte is written after the next row's barrier
+//      (or the final one), which orders it after the owner's 8-byte store.
+// Without kSparse (a layer with more than T channels k != 1, e.g. random-k
+// tests) the masked lanes divide inline instead (ksm bit masks).
+constexpr int kRing = 8;
+template <int T, int V, bool kF16, bool kDyn, bool kSparse>
 __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
                                                   const float* __restrict__ kv, const float* __restrict__ rkv,
-                                                  const uint8_t* __restrict__ kone, int K, int Kpad, int dynamic,
-                                                  float act_scale, int8_t* __restrict__ Q, size_t ldq,
-                                                  float* __restrict__ rs, int M) {
+                                                  const uint8_t* __restrict__ ksm, const int* __restrict__ spec,
+                                                  int nspec, int K, int Kpad, float act_scale,
+                                                  int8_t* __restrict__ Q, size_t ldq, float* __restrict__ rs, int M,
+                                                  int depth) {
   extern __shared__ __align__(128) uint8_t sbuf[];
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ float red[33];
+  __shared__ __align__(8) uint64_t full[kRing];
+  __shared__ float red[2][32];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kEsz = kF16 ? 2 : 4;
+  constexpr int kW = T / 32;
   const uint32_t rowbytes = static_cast<uint32_t>(K) * kEsz;
   const uint32_t bufstride = (rowbytes + 127u) & ~127u;
   const int C8 = K >> 3;
@@ -282,81 +286,151 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
     }
   };
   if (threadIdx.x == 0) {
-    dgqk::mbar_init(&full[0], 1);
-    dgqk::mbar_init(&full[1], 1);
+    for (int b = 0; b < depth; ++b) dgqk::mbar_init(&full[b], 1);
     dgqk::fence_mbar_init();
+    for (int b = 0; b < depth; ++b) {
+      const int r = blockIdx.x + b * gridDim.x;
+      if (r < M) issue(r, b);
+    }
   }
+  const bool special = kSparse && static_cast<int>(threadIdx.x) < nspec;
+  int sj = 0;
+  float sk = 1.0f, srk = 1.0f;
+  if (special) {
+    sj = __ldg(spec + threadIdx.x);
+    sk = __ldg(kv + sj);
+    srk = __ldg(rkv + sj);
+  }
+  int8_t* pend = nullptr;  // the special's code byte of the previous row
+  int pcode = 0;
   __syncthreads();
-  const uint32_t umask = unit_mask<T, V>(kone, static_cast<int>(threadIdx.x), C8);
-  int it = 0;
-  if (threadIdx.x == 0) {
-    if (static_cast<int>(blockIdx.x) < M) issue(blockIdx.x, 0);
-    if (static_cast<int>(blockIdx.x + gridDim.x) < M) issue(blockIdx.x + gridDim.x, 1);
-  }
-  for (int row = blockIdx.x; row < M; row += gridDim.x, ++it) {
-    const int b = it & 1;
-    dgqk::mbar_wait(&full[b], (it >> 1) & 1);
-    const uint8_t* buf = sbuf + b * bufstride;
-    float xv[V][8];
-    float am = 0.0f;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int c = threadIdx.x + v * T;
-      if (c < C8) {
-        const int j = c * 8;
-        float x[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int b = 0, bprev = -1;
+  uint32_t phase = 0;
+  for (int row = blockIdx.x, it = 0; row < M; row += gridDim.x, ++it) {
+    dgqk::mbar_wait(&full[b], phase);
+    uint8_t* buf = sbuf + b * bufstride;
+    float am = 0.0f, xs = 0.0f;
+    if constexpr (kSparse) {
+      if (special) {
         if constexpr (kF16) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(buf + j * 2);
-          const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float2 f = __half22float2(h2[t]);
-            x[2 * t] = f.x;
-            x[2 * t + 1] = f.y;
-          }
+          __half* p = reinterpret_cast<__half*>(buf) + sj;
+          xs = div_k(__half2float(*p), sk, srk);
+          *p = __float2half_rn(0.0f);
         } else {
-          const float4 a = *reinterpret_cast<const float4*>(buf + j * 4);
-          const float4 bb = *reinterpret_cast<const float4*>(buf + j * 4 + 16);
-          x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-          x[4] = bb.x; x[5] = bb.y; x[6] = bb.z; x[7] = bb.w;
+          float* p = reinterpret_cast<float*>(buf) + sj;
+          xs = div_k(*p, sk, srk);
+          *p = 0.0f;
         }
-        smooth_chunk<!kF16, kCheckK>(x, kv, rkv, (umask >> v) & 1u, c, xv[v]);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(xv[v][t]));
+        am = fabsf(xs);
       }
+      __syncthreads();  // specials zeroed in the staged row
     }
+    if constexpr (kDyn) {
+      uint32_t am16 = 0u;
+      uint4 r16[kF16 && kSparse ? V : 1];  // all of the thread's FP16 chunks loaded before any use
+      if constexpr (kF16 && kSparse) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int c = threadIdx.x + v * T;
+          r16[v] = c < C8 ? *reinterpret_cast<const uint4*>(buf + c * 16) : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int c = threadIdx.x + v * T;
+        if (c < C8) {
+          if constexpr (kF16) {
+            const uint4 raw = kSparse ? r16[kSparse ? v : 0] : *reinterpret_cast<const uint4*>(buf + c * 16);
+            if (kSparse || (ksm && !__ldg(ksm + c))) {
+              am16 = __vmaxu2(am16, raw.x & 0x7FFF7FFFu);
+              am16 = __vmaxu2(am16, raw.y & 0x7FFF7FFFu);
+              am16 = __vmaxu2(am16, raw.z & 0x7FFF7FFFu);
+              am16 = __vmaxu2(am16, raw.w & 0x7FFF7FFFu);
+            } else {
+              float x[8];
+              unpack8<true>(&raw, x);
+              smooth_sparse(x, ksm ? __ldg(ksm + c) : 0xFFu, kv, rkv, c * 8);
+#pragma unroll
+              for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(x[t]));
+            }
+          } else {
+            uint4 raw[2];
+            raw[0] = *reinterpret_cast<const uint4*>(buf + c * 32);
+            raw[1] = *reinterpret_cast<const uint4*>(buf + c * 32 + 16);
+            float x[8];
+            unpack8<false>(raw, x);
+            if constexpr (!kSparse) smooth_sparse(x, ksm ? __ldg(ksm + c) : 0xFFu, kv, rkv, c * 8);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) am = fmaxf(am, fabsf(x[t]));
+          }
+        }
+      }
+      if constexpr (kF16) {
+        const float2 m2 = __half22float2(*reinterpret_cast<const __half2*>(&am16));
+        am = fmaxf(am, fmaxf(m2.x, m2.y));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+      if (lane == 0) red[it & 1][warp] = am;
+    }
+    __syncthreads();  // warp maxima published; the previous row's reads and stores retired
+    if (threadIdx.x == 0 && bprev >= 0) {
+      const int nxt = row - static_cast<int>(gridDim.x) + depth * static_cast<int>(gridDim.x);
+      if (nxt < M) issue(nxt, bprev);
+    }
+    if (kSparse && pend) *pend = static_cast<int8_t>(pcode);
     float s = act_scale;
-    if (dynamic) {
-      s = dynamic_row_scale(block_max<T>(am, red));  // its barriers also retire every read of buf
-    } else {
-      __syncthreads();
+    if constexpr (kDyn) {
+      float w = lane < kW ? red[it & 1][lane] : 0.0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
+      s = dynamic_row_scale(w);
     }
-    if (threadIdx.x == 0) {
-      rs[row] = s;
-      const int nxt = row + 2 * gridDim.x;
-      if (nxt < M) issue(nxt, b);
-    }
-    uint2* qr = reinterpret_cast<uint2*>(Q + static_cast<size_t>(row) * ldq);
+    if (threadIdx.x == 0) rs[row] = s;
+    int8_t* qrow = Q + static_cast<size_t>(row) * ldq;
+    uint2* qr = reinterpret_cast<uint2*>(qrow);
     const bool safe = scale_is_safe(s);
     const float inv = __frcp_rn(s);
+    // pass 2 (FP16 rows in groups of 4 chunks: the group's shared-memory loads
+    // are all issued before the first conversion)
+    constexpr int kG = kF16 ? 4 : 1;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int c = threadIdx.x + v * T;
-      if (c < C8) {
-        int o[8];
-        if (safe) {
-          if (dynamic)
-            quant_chunk<false>(xv[v], s, inv, o);
-          else
-            quant_chunk<true>(xv[v], s, inv, o);
-        } else {
+    for (int v0 = 0; v0 < V; v0 += kG) {
+      uint4 raw[kG][kF16 ? 1 : 2];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) o[t] = quant_code_f64(xv[v][t], s);
+      for (int v = v0; v < v0 + kG && v < V; ++v) {
+        const int c = threadIdx.x + v * T;
+        if (c < C8) {
+          raw[v - v0][0] = *reinterpret_cast<const uint4*>(buf + c * 8 * kEsz);
+          if constexpr (!kF16) raw[v - v0][1] = *reinterpret_cast<const uint4*>(buf + c * 32 + 16);
         }
-        qr[c] = make_uint2(pack4(o[0], o[1], o[2], o[3]), pack4(o[4], o[5], o[6], o[7]));
+      }
+#pragma unroll
+      for (int v = v0; v < v0 + kG && v < V; ++v) {
+        const int c = threadIdx.x + v * T;
+        if (c < C8) {
+          float x[8];
+          unpack8<kF16>(raw[v - v0], x);
+          if constexpr (!kSparse) smooth_sparse(x, ksm ? __ldg(ksm + c) : 0xFFu, kv, rkv, c * 8);
+          qr[c] = chunk_codes<!kDyn>(x, s, inv, safe);
+        }
       }
     }
     for (int c = C8 + threadIdx.x; c < (Kpad >> 3); c += T) qr[c] = make_uint2(0u, 0u);
+    if (special) {
+      pend = qrow + sj;
+      pcode = safe ? quant_code_f32(xs, s, inv) : quant_code_f64(xs, s);
+    }
+    bprev = b;
+    if (++b == depth) {
+      b = 0;
+      phase ^= 1u;
+    }
+  }
+  if constexpr (kSparse) {
+    __syncthreads();
+    if (pend) *pend = static_cast<int8_t>(pcode);
   }
 }
 
@@ -380,9 +454,9 @@ __global__ void k_div_check(const float* __restrict__ x, const float* __restrict
 using namespace dgqk;
 
 namespace {
-template <int T, int V, int CL, bool F16, bool CK>
+template <int T, int V, int CL, bool F16>
 cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, const float* rk,
-                       const uint8_t* kone, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
+                       const uint8_t* ksm, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
                        float* rs, int M, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(M) * CL);
@@ -395,14 +469,36 @@ cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, co
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = CL > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, CK>, X, ldx, seg, seg_stride, k, rk, kone, K, Kpad,
-                            dynamic, act_scale, Q, ldq, rs, M);
+  if (dynamic)
+    return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, true>, X, ldx, seg, seg_stride, k, rk, ksm, K, Kpad,
+                              act_scale, Q, ldq, rs, M);
+  return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, false>, X, ldx, seg, seg_stride, k, rk, ksm, K, Kpad,
+                            act_scale, Q, ldq, rs, M);
 }
 }  // namespace
 
+// tools: DGQ_K1_DEPTH=3..8 row buffers and DGQ_K1_T=128|256|512 threads per
+// K1 v3 CTA (A/B runs; 0 = the planner's choice)
+static int aq_depth() {
+  static const int v = [] {
+    const char* e = getenv("DGQ_K1_DEPTH");
+    const int d = e ? atoi(e) : 0;
+    return d <= 0 ? 0 : (d < 3 ? 3 : (d > kRing ? kRing : d));
+  }();
+  return v;
+}
+static int aq_threads() {
+  static const int v = [] {
+    const char* e = getenv("DGQ_K1_T");
+    const int t = e ? atoi(e) : 0;
+    return (t == 128 || t == 256 || t == 512) ? t : 0;
+  }();
+  return v;
+}
+
 cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, size_t seg_stride, const float* k,
                                  const float* rk, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
-                                 float* rs, int M, cudaStream_t st, bool k_checked, const uint8_t* kone) {
+                                 float* rs, int M, cudaStream_t st, const uint8_t* ksm, const int* spec, int nspec) {
   if (M <= 0) return cudaSuccess;
   if (seg <= 0) seg = K;
   const size_t align = f16 ? 8 : 4;  // elements per 16 bytes
@@ -427,38 +523,62 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t stage = 2 * ((static_cast<size_t>(K) * (f16 ? 2 : 4) + 127) & ~size_t(127));
-  if (M >= n_sm && C8 <= 4096 && stage <= 220 * 1024) {
-#define DGQ_AQ3(T_, V_)                                                                                         \
+  const size_t bufstride = (static_cast<size_t>(K) * (f16 ? 2 : 4) + 127) & ~size_t(127);
+  if (M >= n_sm && C8 <= 16 * 512 && 3 * bufstride <= 220 * 1024) {
+    // persistent CTAs of T threads, V <= 16 chunks per thread, `depth` row buffers
+    int T = aq_threads();
+    if (!T) T = C8 <= 8 * 256 ? 256 : 512;  // measured (tools/k1_ab.py): <= 8 chunks per thread
+    while ((C8 + T - 1) / T > 16) T *= 2;
+    const int need = (C8 + T - 1) / T;
+    int depth = aq_depth();
+    if (!depth) depth = 3;
+    while (depth > 3 && depth * bufstride > 220 * 1024) --depth;
+    const size_t smem = depth * bufstride;
+#define DGQ_AQ3_K(T_, V_, F_, D_, S_)                                                                          \
   {                                                                                                             \
-    auto kern = f16 ? (k_checked ? k_actquant3<T_, V_, true, false> : k_actquant3<T_, V_, true, true>)          \
-                    : (k_checked ? k_actquant3<T_, V_, false, false> : k_actquant3<T_, V_, false, true>);       \
-    { cudaError_t e_ = dgq_allow_smem(kern, stage); if (e_ != cudaSuccess) return e_; }                       \
+    auto kern = k_actquant3<T_, V_, F_, D_, S_>;                                                                \
+    { cudaError_t e_ = dgq_allow_smem(kern, smem); if (e_ != cudaSuccess) return e_; }                        \
     int occ = 1;                                                                                                \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, stage);                                       \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, smem);                                        \
     const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \
-    kern<<<grid, T_, stage, st>>>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic, act_scale, Q, ldq, rs, M);  \
+    kern<<<grid, T_, smem, st>>>(X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K, Kpad, act_scale, Q, ldq, rs, \
+                                 M, depth);                                                                     \
     return cudaGetLastError();                                                                                  \
   }
-    if (C8 <= 256) DGQ_AQ3(256, 1)
-    if (C8 <= 512) DGQ_AQ3(256, 2)
-    if (C8 <= 1024) DGQ_AQ3(256, 4)
-    if (C8 <= 2048) DGQ_AQ3(512, 4)
-    // one row per CTA fills the smem (114 KB double-buffered at K = 28672 FP16):
-    // 32 warps instead of 16 hide the per-row latency (fc2 input 69.7 -> 65.5 us;
-    // the same widening slowed 7168-wide rows, tools/k1_time.py)
-    DGQ_AQ3(1024, 4)
-#undef DGQ_AQ3
+#define DGQ_AQ3_S(T_, V_, F_, D_)                                                                               \
+  {                                                                                                             \
+    if (ksm && nspec <= T_) DGQ_AQ3_K(T_, V_, F_, D_, true)                                                     \
+    DGQ_AQ3_K(T_, V_, F_, D_, false)                                                                            \
   }
-#define DGQ_AQ(T_, V_, CL_)                                                                                    \
-  e = f16 ? (k_checked ? launch_aq2<T_, V_, CL_, true, false>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,    \
-                                                               act_scale, Q, ldq, rs, M, st)                     \
-                       : launch_aq2<T_, V_, CL_, true, true>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,     \
-                                                              act_scale, Q, ldq, rs, M, st))                     \
-          : (k_checked ? launch_aq2<T_, V_, CL_, false, false>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,   \
-                                                                act_scale, Q, ldq, rs, M, st)                    \
-                       : launch_aq2<T_, V_, CL_, false, true>(X, ldx, seg, seg_stride, k, rk, kone, K, Kpad, dynamic,    \
-                                                               act_scale, Q, ldq, rs, M, st))
+#define DGQ_AQ3(T_, V_)                                                                                         \
+  {                                                                                                             \
+    if (f16) {                                                                                                  \
+      if (dynamic) DGQ_AQ3_S(T_, V_, true, true)                                                                \
+      DGQ_AQ3_S(T_, V_, true, false)                                                                            \
+    }                                                                                                           \
+    if (dynamic) DGQ_AQ3_S(T_, V_, false, true)                                                                 \
+    DGQ_AQ3_S(T_, V_, false, false)                                                                             \
+  }
+#define DGQ_AQ3_V(T_)                                                                                           \
+  {                                                                                                             \
+    if (need <= 4) DGQ_AQ3(T_, 4)                                                                               \
+    if (need <= 8) DGQ_AQ3(T_, 8)                                                                               \
+    if (need <= 12) DGQ_AQ3(T_, 12)                                                                             \
+    DGQ_AQ3(T_, 16)                                                                                             \
+  }
+    if (T == 128) DGQ_AQ3_V(128)
+    if (T == 256) DGQ_AQ3_V(256)
+    DGQ_AQ3_V(512)
+#undef DGQ_AQ3_V
+#undef DGQ_AQ3
+#undef DGQ_AQ3_S
+#undef DGQ_AQ3_K
+  }
+#define DGQ_AQ(T_, V_, CL_)                                                                                   \
+  e = f16 ? launch_aq2<T_, V_, CL_, true>(X, ldx, seg, seg_stride, k, rk, ksm, K, Kpad, dynamic, act_scale, Q, ldq, \
+                                           rs, M, st)                                                            \
+          : launch_aq2<T_, V_, CL_, false>(X, ldx, seg, seg_stride, k, rk, ksm, K, Kpad, dynamic, act_scale, Q,     \
+                                            ldq, rs, M, st)
   if (C8 <= 128) DGQ_AQ(128, 1, 1);
   else if (C8 <= 256) DGQ_AQ(128, 2, 1);
   else if (C8 <= 512) DGQ_AQ(128, 4, 1);

@@ -146,8 +146,9 @@ struct dgq_layer {
   float* s1 = nullptr;       // [o] (this shard)
   float* k = nullptr;        // [h]
   float* rk = nullptr;       // [h] RN(1/k): hoisted reciprocals for K1
-  bool k_fast = false;       // every k <= 2^24: K1 skips the per-chunk k range check
-  uint8_t* kone = nullptr;   // [h/8] chunk c's eight k are all exactly 1 (K1 skips their division)
+  uint8_t* ksm = nullptr;    // [h/8] bit t of chunk c: k[8c + t] != 1 (only those channels divide in K1)
+  int* spec = nullptr;       // [nspec] the channels with k != 1, ascending
+  int nspec = 0;
   size_t device_bytes = 0;
   CUtensorMap tmA{};  // non-fused A operand
   // Internal split-K workspaces for callers that pass none, one per stream:
@@ -327,7 +328,8 @@ void dgq_layer_destroy(dgq_layer* L) {
   cudaFree(L->s1);
   cudaFree(L->k);
   cudaFree(L->rk);
-  cudaFree(L->kone);
+  cudaFree(L->ksm);
+  cudaFree(L->spec);
   for (auto& kv : L->ws) {
     cudaFree(kv.second.p);
     if (kv.second.ev) cudaEventDestroy(kv.second.ev);
@@ -405,18 +407,24 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
   DGQ_CUDA_L(cudaMemcpyAsync(L->s1, s1 + col_begin, L->o * sizeof(float), cudaMemcpyHostToDevice, st));
   DGQ_CUDA_L(cudaMemcpyAsync(L->k, k, h * sizeof(float), cudaMemcpyHostToDevice, st));
   DGQ_CUDA_L(cudaMalloc(&L->rk, h * sizeof(float)));
-  L->k_fast = true;
-  for (size_t j = 0; j < h; ++j) L->k_fast = L->k_fast && k[j] <= 0x1p24f;
   DGQ_CUDA_L(dgq_launch_reciprocal(L->k, L->rk, static_cast<int>(h), st));
   if (h % 8 == 0) {
-    std::vector<uint8_t> kone(h / 8);
+    std::vector<uint8_t> ksm(h / 8);
     for (size_t c = 0; c < h / 8; ++c) {
-      bool one = true;
-      for (size_t t = 0; t < 8; ++t) one = one && k[c * 8 + t] == 1.0f;
-      kone[c] = one ? 1 : 0;
+      uint8_t m = 0;
+      for (size_t t = 0; t < 8; ++t) m |= (k[c * 8 + t] != 1.0f ? 1u : 0u) << t;
+      ksm[c] = m;
     }
-    DGQ_CUDA_L(cudaMalloc(&L->kone, h / 8));
-    DGQ_CUDA_L(cudaMemcpy(L->kone, kone.data(), h / 8, cudaMemcpyHostToDevice));
+    DGQ_CUDA_L(cudaMalloc(&L->ksm, h / 8));
+    DGQ_CUDA_L(cudaMemcpy(L->ksm, ksm.data(), h / 8, cudaMemcpyHostToDevice));
+    std::vector<int> spec;
+    for (size_t j = 0; j < h; ++j)
+      if (k[j] != 1.0f) spec.push_back(static_cast<int>(j));
+    L->nspec = static_cast<int>(spec.size());
+    if (!spec.empty()) {
+      DGQ_CUDA_L(cudaMalloc(&L->spec, spec.size() * sizeof(int)));
+      DGQ_CUDA_L(cudaMemcpy(L->spec, spec.data(), spec.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
   }
   L->device_bytes = (L->o + h) * sizeof(float);
   if (L->fused) {
@@ -572,7 +580,7 @@ dgq_status dgq_quantize_act_f16(const dgq_layer* L, const void* dX, size_t M, si
   if (seg_cols && seg_stride < M * ldx) return fail(DGQ_EINVAL, "seg_stride smaller than one shard");
   DGQ_CUDA(dgq_launch_actquant2(dX, true, ldx, static_cast<int>(seg), seg_stride, L->k, L->rk,
                                 static_cast<int>(L->h), static_cast<int>(ldq), L->mode, L->act_scale, dXq, ldq,
-                                dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast, L->kone));
+                                dRowScale, static_cast<int>(M), static_cast<cudaStream_t>(stream), L->ksm, L->spec, L->nspec));
   return DGQ_OK;
 }
 
@@ -585,7 +593,7 @@ dgq_status dgq_quantize_act(const dgq_layer* L, const float* dX, size_t M, size_
   if (M > 0x7FFFFFFF) return fail(DGQ_EINVAL, "too many rows");
   DGQ_CUDA(dgq_launch_actquant2(dX, false, ldx, static_cast<int>(L->h), 0, L->k, L->rk, static_cast<int>(L->h),
                                 static_cast<int>(ldq), L->mode, L->act_scale, dXq, ldq, dRowScale,
-                                static_cast<int>(M), static_cast<cudaStream_t>(stream), L->k_fast, L->kone));
+                                static_cast<int>(M), static_cast<cudaStream_t>(stream), L->ksm, L->spec, L->nspec));
   return DGQ_OK;
 }
 

@@ -143,8 +143,10 @@ cudaError_t dgq_launch_gemm(const DgqGemmPlan& plan, bool fused, const CUtensorM
 // rk = RN(1/k) per input channel (dgq_launch_reciprocal).
 cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, size_t seg_stride, const float* k,
                                  const float* rk, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
-                                 float* rs, int M, cudaStream_t st, bool k_checked = false,
-                                 const uint8_t* kone = nullptr);  // kone[c]: channels 8c..8c+7 all have k == 1
+                                 float* rs, int M, cudaStream_t st,
+                                 const uint8_t* ksm = nullptr,  // ksm[c] bit t: k[8c + t] != 1
+                                 const int* spec = nullptr,     // the channels with k != 1, ascending
+                                 int nspec = 0);
 cudaError_t dgq_launch_reciprocal(const float* k, float* rk, int n, cudaStream_t st);
 cudaError_t dgq_launch_div_check(const float* x, const float* k, float* fast, float* ieee, int n, cudaStream_t st);
 
