@@ -209,6 +209,13 @@ dgq_status dgq_phase2_search(const float* dW, size_t h, size_t o, const float* d
                              size_t n_alpha, float* dS1, int8_t* dS2, int32_t* dCodes, double* dColErr,
                              float* dColAlpha, uint64_t* evals, void* stream);
 
+/* ---- measured dense INT8 tensor peak ----------------------------------------
+ * The INT8 roofline denominator: every SM pair issues
+ * tcgen05.mma.cta_group::2.kind::i8 (256 x 256 x 32, K5p's shape) back to back
+ * from shared-memory operands; best of `reps` launches (CUDA events), TOPS out.
+ * Synchronises; runs on the current device. */
+dgq_status dgq_measure_i8_peak(int reps, double* tops, double* best_ms);
+
 /* ---- host-buffer API: the reference's calling convention --------------------
  * Host arrays in (reference layouts), host arrays out; each call uploads,
  * runs the CUDA kernels on a per-thread stream of the CURRENT device and

@@ -88,6 +88,7 @@ _SIGS = {
                                C.POINTER(C.c_uint64), _vp]),
     "dgq_phase2_search": (_i, [_vp, _sz, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp,
                                C.POINTER(C.c_uint64), _vp]),
+    "dgq_measure_i8_peak": (_i, [_i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     # host-buffer API (the reference's calling convention)
     "dgq_host_quantize_activations": (_i, [_vp, _sz, _sz, _vp, _i, _f, _vp, _vp]),
     "dgq_host_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp]),

@@ -259,6 +259,31 @@ class CudaLayer:
 
     __call__ = forward
 
+    def forward_device(self, x: torch.Tensor, bias: torch.Tensor | None = None, out_dtype=torch.float16):
+        """K1 + K5 through the single C-ABI call dgq_forward_device (x: cuda float32 [M, h])."""
+        assert x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 and x.stride(1) == 1
+        M = x.shape[0]
+        y = torch.empty(M, self.o, dtype=out_dtype, device=x.device)
+        codes = torch.empty(M, self.k_pad, dtype=torch.int8, device=x.device)
+        rs = torch.empty(M, dtype=torch.float32, device=x.device)
+        od = OUT_F16 if out_dtype == torch.float16 else OUT_F32
+        check(lib().dgq_forward_device(self._h, _t_ptr(x), M, x.stride(0), _t_ptr(bias), od, _t_ptr(y), y.stride(0),
+                                       _t_ptr(codes), _t_ptr(rs), None, 0, _stream(x.device)))
+        return y
+
+    def forward_host(self, X: np.ndarray, bias: torch.Tensor | None = None, out_dtype=np.float16) -> np.ndarray:
+        """The serving call with HOST buffers (dgq_layer_forward_host): X float32
+        [M, h] in host memory -> Y [M, o] host array; token chunks pipeline their
+        copies under the kernels.  Pass page-locked X for full PCIe bandwidth."""
+        X = np.ascontiguousarray(X, np.float32)
+        assert X.ndim == 2 and X.shape[1] == self.h
+        Y = np.empty((X.shape[0], self.o), np.float16 if out_dtype == np.float16 else np.float32)
+        od = OUT_F16 if out_dtype == np.float16 else OUT_F32
+        with torch.cuda.device(self.device):
+            check(lib().dgq_layer_forward_host(self._h, _np_ptr(X), X.shape[0], _t_ptr(bias), od, _np_ptr(Y),
+                                               _stream(self.device)))
+        return Y
+
     # K2s from the prepared tiles
     def dequant_s8(self) -> torch.Tensor:
         w = torch.empty(self.h, self.o, dtype=torch.int8, device=f"cuda:{self.device}")

@@ -1073,4 +1073,40 @@ dgq_status dgq_phase2_search(const float* dW, size_t h, size_t o, const float* d
   return DGQ_OK;
 }
 
+// ---- measured INT8 tensor peak (the roofline denominator) ----
+dgq_status dgq_measure_i8_peak(int reps, double* tops, double* best_ms) {
+  if (!tops) return fail(DGQ_EINVAL, "null argument");
+  int dev = 0, sms = 148;
+  DGQ_CUDA(cudaGetDevice(&dev));
+  DGQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int pairs = sms / 2, blocks = 4096;
+  unsigned long long* sink = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  DGQ_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DGQ_CUDA(cudaMalloc(&sink, sizeof(unsigned long long)));
+  DGQ_CUDA(cudaEventCreate(&e0));
+  DGQ_CUDA(cudaEventCreate(&e1));
+  float best = 1e30f;
+  cudaError_t e = dgq_launch_i8_peak(pairs, blocks, sink, st);  // warm-up
+  for (int i = 0; e == cudaSuccess && i < (reps > 0 ? reps : 10); ++i) {
+    cudaEventRecord(e0, st);
+    e = dgq_launch_i8_peak(pairs, blocks, sink, st);
+    cudaEventRecord(e1, st);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float ms = 0.0f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    if (e == cudaSuccess && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  cudaStreamDestroy(st);
+  DGQ_CUDA(e);
+  const double ops = 2.0 * 256 * 256 * 32 * 4.0 * blocks * pairs;
+  *tops = ops / (best * 1e-3) / 1e12;
+  if (best_ms) *best_ms = best;
+  return DGQ_OK;
+}
+
 }  // extern "C"

@@ -8,6 +8,7 @@
 // memory pool (kept cached between calls).  There is no CPU compute here.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -102,6 +103,44 @@ dgq_status download(void* host, const DevBuf& b, size_t n, cudaStream_t st) {
 }
 
 size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+// Per-thread copy streams and events of the serving call's pipeline (one set
+// per host thread and device).
+struct CopyLanes {
+  int dev = -1;
+  cudaStream_t in = nullptr, out = nullptr;
+  static constexpr int kEv = 16;
+  cudaEvent_t ev_in[kEv] = {}, ev_c[kEv] = {};
+  ~CopyLanes() { release(); }
+  void release() {
+    if (in) cudaStreamDestroy(in);
+    if (out) cudaStreamDestroy(out);
+    for (int i = 0; i < kEv; ++i) {
+      if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+      if (ev_c[i]) cudaEventDestroy(ev_c[i]);
+      ev_in[i] = ev_c[i] = nullptr;
+    }
+    in = out = nullptr;
+  }
+};
+thread_local CopyLanes t_lanes;
+
+dgq_status copy_lanes(CopyLanes** out) {
+  int dev = 0;
+  DGQ_H_CUDA(cudaGetDevice(&dev));
+  if (t_lanes.dev != dev || !t_lanes.in) {
+    t_lanes.release();
+    DGQ_H_CUDA(cudaStreamCreateWithFlags(&t_lanes.in, cudaStreamNonBlocking));
+    DGQ_H_CUDA(cudaStreamCreateWithFlags(&t_lanes.out, cudaStreamNonBlocking));
+    for (int i = 0; i < CopyLanes::kEv; ++i) {
+      DGQ_H_CUDA(cudaEventCreateWithFlags(&t_lanes.ev_in[i], cudaEventDisableTiming));
+      DGQ_H_CUDA(cudaEventCreateWithFlags(&t_lanes.ev_c[i], cudaEventDisableTiming));
+    }
+    t_lanes.dev = dev;
+  }
+  *out = &t_lanes;
+  return DGQ_OK;
+}
 
 bool shape_ok(size_t h, size_t o, size_t g) { return h && o && o % 2 == 0 && g && h % g == 0; }
 
@@ -305,15 +344,44 @@ dgq_status dgq_layer_forward_host(const dgq_layer* layer, const float* X, size_t
   DGQ_H_TRY(dgq_layer_get_info(layer, &info));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (!st) DGQ_H_TRY(host_stream(&st));
+  CopyLanes* ln = nullptr;
+  DGQ_H_TRY(copy_lanes(&ln));
   const size_t esz = out_dtype == DGQ_OUT_F16 ? 2 : 4;
+  // Token chunks: chunk c's input copy (lane `in`), K1 + K5 (the caller's stream)
+  // and output copy (lane `out`) are ordered by events, so copies of one chunk
+  // run under the kernels of its neighbours (PCIe is full duplex).  Small
+  // calls are one chunk.  Scratch comes from the stream-ordered pool.
+  size_t chunk = M <= 256 ? M : round_up((M + 3) / 4, 128);
+  const int nch = static_cast<int>((M + chunk - 1) / chunk);
+  if (nch > CopyLanes::kEv) chunk = round_up((M + CopyLanes::kEv - 1) / CopyLanes::kEv, 128);
   DevBuf dx, dq, dr, dy;
-  DGQ_H_TRY(upload(dx, X, M * info.h * sizeof(float), st));
+  DGQ_H_CUDA(dx.alloc(M * info.h * sizeof(float), st));
   DGQ_H_CUDA(dq.alloc(M * info.k_pad, st));
   DGQ_H_CUDA(dr.alloc(M * sizeof(float), st));
   DGQ_H_CUDA(dy.alloc(M * info.o * esz, st));
-  DGQ_H_TRY(dgq_forward_device(layer, dx.as<float>(), M, info.h, dBias, out_dtype, dy.p, info.o, dq.as<int8_t>(),
-                               dr.as<float>(), nullptr, 0, st));
-  DGQ_H_TRY(download(Y, dy, M * info.o * esz, st));
+  // the copy lanes must not run ahead of the pool allocations made on `st`
+  DGQ_H_CUDA(cudaEventRecord(ln->ev_c[0], st));
+  DGQ_H_CUDA(cudaStreamWaitEvent(ln->in, ln->ev_c[0], 0));
+  DGQ_H_CUDA(cudaStreamWaitEvent(ln->out, ln->ev_c[0], 0));
+  int c = 0;
+  for (size_t r0 = 0; r0 < M; r0 += chunk, ++c) {
+    const size_t m = std::min(chunk, M - r0);
+    DGQ_H_CUDA(cudaMemcpyAsync(dx.as<float>() + r0 * info.h, X + r0 * info.h, m * info.h * sizeof(float),
+                               cudaMemcpyHostToDevice, ln->in));
+    DGQ_H_CUDA(cudaEventRecord(ln->ev_in[c], ln->in));
+    DGQ_H_CUDA(cudaStreamWaitEvent(st, ln->ev_in[c], 0));
+    DGQ_H_TRY(dgq_forward_device(layer, dx.as<float>() + r0 * info.h, m, info.h, dBias, out_dtype,
+                                 static_cast<uint8_t*>(dy.p) + r0 * info.o * esz, info.o,
+                                 dq.as<int8_t>() + r0 * info.k_pad, dr.as<float>() + r0, nullptr, 0, st));
+    DGQ_H_CUDA(cudaEventRecord(ln->ev_c[c], st));
+    DGQ_H_CUDA(cudaStreamWaitEvent(ln->out, ln->ev_c[c], 0));
+    DGQ_H_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(Y) + r0 * info.o * esz,
+                               static_cast<uint8_t*>(dy.p) + r0 * info.o * esz, m * info.o * esz,
+                               cudaMemcpyDeviceToHost, ln->out));
+  }
+  // the scratch is released on `st` once the output copies are done
+  DGQ_H_CUDA(cudaEventRecord(ln->ev_in[0], ln->out));
+  DGQ_H_CUDA(cudaStreamWaitEvent(st, ln->ev_in[0], 0));
   DGQ_H_CUDA(cudaStreamSynchronize(st));
   return DGQ_OK;
 }

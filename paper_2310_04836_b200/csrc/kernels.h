@@ -162,6 +162,10 @@ cudaError_t dgq_launch_phase2(const float* W, const float* X, const float* Xhat,
                               double* ref, double* err, float* s1, int8_t* s2, int32_t* codes, double* col_err,
                               float* col_alpha, cudaStream_t st);
 
+// Dense INT8 tensor peak microbenchmark (csrc/peak.cu): `pairs` SM pairs, each
+// issuing `blocks` x 4 tcgen05.mma.cta_group::2.kind::i8 of 256 x 256 x 32.
+cudaError_t dgq_launch_i8_peak(int pairs, int blocks, unsigned long long* sink, cudaStream_t st);
+
 // Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum,
 // once per (kernel, device) under a lock, so concurrent launches of one
 // instantiation with different sizes never shrink each other's limit.

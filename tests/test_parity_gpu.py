@@ -656,3 +656,24 @@ def test_shared_layer_concurrent_streams_internal_workspace(cuda, port, decode_k
     for i in range(2):
         for y in outs[i]:
             assert np.array_equal(bits(y.cpu().numpy()), bits(refs[i]))
+
+
+@pytest.mark.parametrize("M", [1, 37, 300, 1100])
+def test_serving_calls_match_oracle(cuda, port, M):
+    # dgq_forward_device (K1 + K5 in one C-ABI call) and dgq_layer_forward_host
+    # (host buffers in and out, token chunks pipelined over two copy streams)
+    # against the oracle: FP32 bit-exact, FP16 == fp16_round(FP32)
+    h, o = 1024, 384
+    L = oracle.random_layer(h, o, 128, seed=M + 5)
+    X = port.gen_synthetic(M, h, 70 + M, 3, 50.0, 3)
+    bias = np.random.default_rng(M).uniform(-0.5, 0.5, o).astype(np.float32)
+    out, *_ = port.dgq_forward(X, L, bias)
+    CL = dgq.CudaLayer(_to_dgq(L))
+    db = torch.from_numpy(bias).cuda()
+    y = CL.forward_device(torch.from_numpy(X).cuda(), bias=db, out_dtype=torch.float32)
+    assert np.array_equal(bits(y.cpu().numpy()), bits(out))
+    for _ in range(2):  # cached scratch / events reused
+        Y32 = CL.forward_host(X, bias=db, out_dtype=np.float32)
+        assert np.array_equal(bits(Y32), bits(out))
+        Y16 = CL.forward_host(X, bias=db, out_dtype=np.float16)
+        assert np.array_equal(bits(Y16), bits(oracle.fp16_round_np(out).astype(np.float16)))
