@@ -487,6 +487,14 @@ static int aq_depth() {
   }();
   return v;
 }
+// tools: DGQ_K1_DEC=0 keeps one CTA per row for few-row calls (A/B runs)
+static int aq_decode_clusters() {
+  static const int v = [] {
+    const char* e = getenv("DGQ_K1_DEC");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
 static int aq_threads() {
   static const int v = [] {
     const char* e = getenv("DGQ_K1_T");
@@ -579,7 +587,15 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
                                            rs, M, st)                                                            \
           : launch_aq2<T_, V_, CL_, false>(X, ldx, seg, seg_stride, k, rk, ksm, K, Kpad, dynamic, act_scale, Q,     \
                                             ldq, rs, M, st)
-  if (C8 <= 128) DGQ_AQ(128, 1, 1);
+  // few rows (decode): spread each row over a cluster so every thread owns one
+  // or two chunks — the row's loads are all in flight at once (latency-bound)
+  if (M <= 16 && aq_decode_clusters() && C8 > 256 && C8 <= 4096) {
+    if (C8 <= 512) DGQ_AQ(256, 1, 2);
+    else if (C8 <= 1024) DGQ_AQ(256, 1, 4);
+    else if (C8 <= 2048) DGQ_AQ(256, 1, 8);
+    else DGQ_AQ(256, 2, 8);
+  }
+  else if (C8 <= 128) DGQ_AQ(128, 1, 1);
   else if (C8 <= 256) DGQ_AQ(128, 2, 1);
   else if (C8 <= 512) DGQ_AQ(128, 4, 1);
   else if (C8 <= 1024) DGQ_AQ(256, 4, 1);

@@ -677,3 +677,4 @@ def test_serving_calls_match_oracle(cuda, port, M):
         assert np.array_equal(bits(Y32), bits(out))
         Y16 = CL.forward_host(X, bias=db, out_dtype=np.float16)
         assert np.array_equal(bits(Y16), bits(oracle.fp16_round_np(out).astype(np.float16)))
+
