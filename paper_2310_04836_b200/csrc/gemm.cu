@@ -615,7 +615,7 @@ DgqGemmPlan dgq_plan_gemm(int M, int N, int K_pad, bool fused, int g, int force_
     // q 7168^2 at M = 1024 / 2048 45 / 84 vs 54 / 91 us, 4096^2 at 1024 30 vs 23)
     const long long t512 = ((M + 511) / 512) * static_cast<long long>((N + 255) / 256);
     const bool s2_pays = t512 * kblocks >= 25LL * pairs;
-    pl.pair_sub = (sk && pl.pair_tn == 256 && M >= 512 && (s2_pays || (g_decode_mode & 0x40000000)) &&
+    pl.pair_sub = (sk && M >= 512 && (s2_pays || (g_decode_mode & 0x40000000)) &&
                    (g_decode_mode & 0x20000) == 0 && dgq_prefill2_smem_bytes(cb, 2) <= 232448) ? 2 : 1;
     pl.bn = 256 * pl.pair_sub;
     pl.nt = pl.pair_tn / 128;

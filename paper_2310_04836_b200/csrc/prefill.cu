@@ -51,7 +51,7 @@ namespace pf {
 // cycle falls by S.  S = 2 fills TMEM with one accumulator set (2 x 256
 // columns): the epilogue of a tile no longer overlaps the next tile's main
 // loop, but the dequantisers (now two groups) have twice the time per k-block.
-template <int S>
+template <int S, int TN = 256>
 struct Cfg {
   static constexpr int kSA = S == 1 ? 5 : 3;        // Xq stages (S tiles each, released by the MMA)
   static constexpr int kSC = S == 1 ? 7 : 5;        // packed-chunk stages (released by the dequantisers)
@@ -63,7 +63,9 @@ struct Cfg {
   static constexpr int kEpiWarps = S == 1 ? 4 : 8;
   static constexpr int kXWarp = kEpiWarp0 + kEpiWarps;  // second Xq-tile producer warp
   static constexpr int kThreads = 32 * (kXWarp + 1);
-  static constexpr int kNAcc = 2 / S;               // accumulator sets in TMEM (256 * S columns each)
+  // accumulator sets in TMEM (TN * S columns each): two whenever they fit, so a
+  // tile's epilogue overlaps the next tile's main loop
+  static constexpr int kNAcc = TN * S <= 256 ? 2 : 1;
 };
 constexpr uint32_t kATile = 128 * 128;   // 128 token rows x 128 k (bytes)
 constexpr uint32_t kBTile = 128 * 128;   // 128 channel rows x 128 k
@@ -93,13 +95,12 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-// Per-k-block "stage dequantised" signal to the leader.  A release.cluster
-// arrive costs 0.5-1 us here (measured, tools/pf_trace.py), more than a k-block
-// of MMA, so the signal is relaxed: the 256 dequant threads' st.shared have
-// been drained by the named barrier (bar.sync completes outstanding shared
-// stores) and made visible to the async proxy by fence.proxy.async before
-// the arrive is issued; the leader's tcgen05.mma reads them through the async
-// proxy after observing the arrive.  The bit-exact GPU tests pin this.
+// Per-k-block "stage dequantised" signal to the leader: a relaxed arrive
+// preceded by a cluster-scope release fence restricted to shared::cta (a
+// release pattern; see the dequantiser).
+// The dequant threads' st.shared are made visible to the async proxy by
+// fence.proxy.async and ordered before the fence by the group's named barrier;
+// the leader's tcgen05.mma reads them after its acquire.cluster wait.
 __device__ __forceinline__ void arrive_remote_relaxed(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -117,6 +118,9 @@ __device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t parity)
       : "memory");
   return ok != 0;
 }
+#ifndef DGQ_PF_RELAXED_READY
+#define DGQ_PF_RELAXED_READY 0  // tools: 1 drops the release fence before the ready arrive (A/B of its cost)
+#endif
 #ifndef DGQ_PF_BACKOFF
 #define DGQ_PF_BACKOFF 0
 #endif
@@ -479,17 +483,16 @@ __device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase,
 // prepared tile; twice the tiles, for shapes whose 256-wide tiles leave a
 // ragged last wave).
 template <int TN, int S>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThreads, 1)
     k_dgq_prefill2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmY,
                    const DgqGemmParams p) {
   using namespace pf;
-  using C = Cfg<S>;
+  using C = Cfg<S, TN>;
   constexpr int kSA = C::kSA, kSC = C::kSC, kSB = C::kSB, kDqGroups = C::kDqGroups;
   constexpr int kEpiWarp0 = C::kEpiWarp0, kXWarp = C::kXWarp, kNAcc = C::kNAcc, kEpiWarps = C::kEpiWarps;
   constexpr int kEpiThreads = 32 * kEpiWarps;
   constexpr uint32_t kStaging = kEpiWarps * kStagingPerWarp;
   constexpr uint32_t kAStage = S * kATile;  // one Xq stage: S tiles of 128 token rows
-  static_assert(S == 1 || TN == 256, "two token sub-tiles use the 256-wide pair tile");
   constexpr uint32_t kIdesc = idesc_i8(256, TN);
   constexpr int kRows = TN / 2;  // channel rows of B held (and dequantised) by each CTA
   const uint32_t rank = cluster_rank();
@@ -649,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
           }
         }
         tc_fence_after();
-        const uint32_t d = tm + acc * 256 * S;  // accumulator set: S x (TN <= 256) columns
+        const uint32_t d = tm + acc * TN * S;  // accumulator set: S sub-tiles x TN columns
         for (int kb = lo; kb < hi; ++kb, ++it) {
           const int s = it % kSA, b = it % kSB;
           wait_cluster(&ready[b], (it / kSB) & 1, 3);  // both CTAs' B slots dequantised
@@ -666,7 +669,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
             const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kAStage + sub * kATile));
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma2_i8(d + sub * 256, da + 2 * kk, db + 2 * kk, kIdesc, (kb != lo) || kk != 0);
+              mma2_i8(d + sub * TN, da + 2 * kk, db + 2 * kk, kIdesc, (kb != lo) || kk != 0);
           }
           commit2_mc(&aempty[s]);
           commit2_mc(&bempty[b]);
@@ -744,6 +747,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
         if ((warp & 3) == 0 && lane == 0) {
           pf_stamp(p, 4, it);
           mbar_arrive(&cempty[s]);  // the chunk has been read
+          // Release pattern at cluster scope: the group's B-tile writes happen
+          // before this thread's fence (bar.sync orders them within the CTA), the
+          // fence is cumulative, and the leader's acquire.cluster wait on ready[b]
+          // synchronises with the arrive that follows it, so the peer's rows are
+          // visible to the leader before its tcgen05.mma reads them.
+#if !DGQ_PF_RELAXED_READY
+          // release fence restricted to this CTA's shared memory (the B rows):
+          // MEMBAR.CTA + FENCE.VIEW.ASYNC.S in SASS, where fence.acq_rel.cluster
+          // is a GPU-scope MEMBAR that cost ~20 % of the kernel (tools/pf_ab.py)
+          asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+#endif
           arrive_remote_relaxed(ready_leader + b * 8);  // one per group: leader's ready[b]
         }
       }
@@ -775,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
       // sub-tile `sub` of this CTA: token rows mt*256S + sub*256 + rank*128 + [0, 128)
       auto m0_of = [&](int sub) { return mt * 256 * S + sub * 256 + static_cast<int>(rank) * 128; };
       auto tbase_of = [&](int sub) {
-        return tmem + ((q * 32) << 16) + static_cast<uint32_t>(acc * 256 * S + sub * 256);
+        return tmem + ((q * 32) << 16) + static_cast<uint32_t>(acc * TN * S + sub * TN);
       };
       if (lo > 0) {
         // stream-K contributor: park the int32 partials in this pair's slot
@@ -959,9 +973,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S>::kThreads
 
 using namespace dgqk;
 
-template <int S>
+template <int S, int TN = 256>
 static size_t smem_bytes_s(uint32_t chunk_stride) {
-  using C = pf::Cfg<S>;
+  using C = pf::Cfg<S, TN>;
   return 1024 + static_cast<size_t>(C::kSA) * S * pf::kATile + C::kSC * chunk_stride + C::kSB * pf::kBTile +
          C::kEpiWarps * pf::kStagingPerWarp + (2 * C::kSA + 2 * C::kSC + 2 * C::kSB + 5) * 8 + 32 +
          (128 * S + 256 + 256) * 4;
@@ -980,13 +994,13 @@ static int max_active_pairs() {
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int n = sms / 2;
-  const size_t smem = smem_bytes_s<S>(static_cast<uint32_t>(dgq_layout::chunk_bytes(128)));
+  const size_t smem = smem_bytes_s<S, TN>(static_cast<uint32_t>(dgq_layout::chunk_bytes(128)));
   auto kern = k_dgq_prefill2<TN, S>;
   if (dgq_allow_smem(kern, smem) ==
       cudaSuccess) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * n);
-    cfg.blockDim = dim3(pf::Cfg<S>::kThreads);
+    cfg.blockDim = dim3(pf::Cfg<S, TN>::kThreads);
     cfg.dynamicSmemBytes = smem;
     int q = 0;
     if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0 && q < n) n = q;
@@ -997,7 +1011,7 @@ static int max_active_pairs() {
 }
 
 int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int sub) {
-  const int pairs = sub == 2 ? max_active_pairs<256, 2>()
+  const int pairs = sub == 2 ? (tn == 128 ? max_active_pairs<128, 2>() : max_active_pairs<256, 2>())
                              : (tn == 128 ? max_active_pairs<128, 1>() : max_active_pairs<256, 1>());
   const long long tiles = static_cast<long long>((M + 256 * sub - 1) / (256 * sub)) * ((N + tn - 1) / tn);
   const long long work = stream_k ? tiles * k_blocks : tiles;
@@ -1022,13 +1036,13 @@ int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int
 template <int TN, int S>
 static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
                              cudaStream_t st) {
-  const size_t smem = smem_bytes_s<S>(p.chunk_stride);
+  const size_t smem = smem_bytes_s<S, TN>(p.chunk_stride);
   auto kern = k_dgq_prefill2<TN, S>;
   cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN, p.k_blocks, p.stream_k != 0, S));
-  cfg.blockDim = dim3(pf::Cfg<S>::kThreads);
+  cfg.blockDim = dim3(pf::Cfg<S, TN>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -1043,6 +1057,6 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
 
 cudaError_t dgq_launch_prefill2(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, int tn,
                                 int sub, bool pdl, cudaStream_t st) {
-  if (sub == 2) return launch_pf<256, 2>(tmA, tmY, p, pdl, st);
+  if (sub == 2) return tn == 128 ? launch_pf<128, 2>(tmA, tmY, p, pdl, st) : launch_pf<256, 2>(tmA, tmY, p, pdl, st);
   return tn == 128 ? launch_pf<128, 1>(tmA, tmY, p, pdl, st) : launch_pf<256, 1>(tmA, tmY, p, pdl, st);
 }

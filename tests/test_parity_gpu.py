@@ -336,7 +336,7 @@ PREFILL_CASES = [
 # 0x20000 one token sub-tile per CTA (256-token pair tiles), 0x40000000 two from M >= 512
 # (otherwise the planner picks by work per pair)
 PAIR_MODES = {"sk256": 0x400, "sk256s1": 0x400 | 0x20000, "sk256s2": 0x400 | 0x40000000, "sk128": 0x400 | 0x800,
-              "rr256": 0x400 | 0x2000,
+              "sk128s2": 0x400 | 0x800 | 0x40000000, "rr256": 0x400 | 0x2000,
               "rr128": 0x400 | 0x800 | 0x2000}
 
 
@@ -678,3 +678,39 @@ def test_serving_calls_match_oracle(cuda, port, M):
         Y16 = CL.forward_host(X, bias=db, out_dtype=np.float16)
         assert np.array_equal(bits(Y16), bits(oracle.fp16_round_np(out).astype(np.float16)))
 
+
+
+def test_prefill_pair_kernel_stress_10k_launches(cuda, port):
+    # 10^4 launches of the CTA-pair kernel (K5p) over five shapes and both token
+    # sub-tilings, every output compared bit for bit with the first (on the GPU)
+    # and the first with the oracle: the cross-CTA ready signal, stream-K flags
+    # and partial slots must be exact on every launch.
+    import ctypes
+
+    lib = dgq.lib()
+    lib.dgq_debug_set_decode.argtypes = [ctypes.c_int]
+    rng = np.random.default_rng(2024)
+    cases = [(512, 2048, 1024), (777, 1024, 768), (1024, 4096, 512), (300, 1536, 1280), (2048, 1024, 512)]
+    launches = 0
+    try:
+        for i, (M, h, o) in enumerate(cases):
+            L = oracle.random_layer(h, o, 128, seed=900 + i)
+            X = port.gen_synthetic(M, h, 40 + i, 3, 50.0, 3)
+            out, *_ = port.dgq_forward(X, L)
+            CL = dgq.CudaLayer(_to_dgq(L))
+            codes, drs = CL.quantize_act(torch.from_numpy(X).cuda())
+            for mode in (1 | 0x400, 1 | 0x400 | 0x40000000, 1 | 0x400 | 0x20000):
+                lib.dgq_debug_set_decode(mode)
+                ref = CL.linear(codes, drs, out_dtype=torch.float32)
+                assert np.array_equal(bits(ref.cpu().numpy()), bits(out)), (M, h, o, hex(mode))
+                y = torch.empty_like(ref)
+                bad = torch.zeros((), dtype=torch.int64, device=ref.device)
+                n = int(rng.integers(600, 750))
+                for _ in range(n):
+                    CL.linear(codes, drs, out=y)
+                    bad += (y.view(torch.int32) != ref.view(torch.int32)).sum()
+                launches += n
+                assert int(bad) == 0, (M, h, o, hex(mode))
+    finally:
+        lib.dgq_debug_set_decode(1)
+    assert launches >= 10_000
