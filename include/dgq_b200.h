@@ -17,6 +17,7 @@
  *   DGQ_EVALIDATION -> dgq::validation_error   (proj/src/format.cpp:18-20,131-136)
  *   DGQ_EOVERFLOW   -> std::runtime_error      (proj/src/kernel.cpp:83-85)
  *   DGQ_EFORMAT     -> dgq::format_error       (proj/src/format.cpp:214-250)
+ *   DGQ_EIO         -> dgq::io_error           (proj/src/format.cpp:268-290)
  */
 #ifndef DGQ_B200_H
 #define DGQ_B200_H
@@ -37,7 +38,8 @@ typedef enum dgq_status {
   DGQ_EOVERFLOW = 3,
   DGQ_ECUDA = 4,
   DGQ_ENOMEM = 5,
-  DGQ_EFORMAT = 6
+  DGQ_EFORMAT = 6,
+  DGQ_EIO = 7
 } dgq_status;
 
 enum { DGQ_MODE_STATIC = 0, DGQ_MODE_DYNAMIC = 1 };      /* proj/include/dgq/format.hpp:32 ActMode */
@@ -91,6 +93,12 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
  * proj/src/format.cpp:214-266) straight to a prepared (sharded) layer. */
 dgq_status dgq_layer_create_from_dgq1(int device, const uint8_t* bytes, size_t nbytes, size_t col_begin,
                                       size_t col_end, void* stream, dgq_layer** out);
+/* The same from a DGQ1 FILE, streamed: S2 / ZP / s1 / k are read first, then
+ * the code rows in ~32 MB slabs through pinned buffers, validated on the GPU
+ * and repacked (only the shard's columns are uploaded).  DGQ_EIO (dgq::io_error)
+ * when the file cannot be opened or read. */
+dgq_status dgq_layer_create_from_dgq1_file(int device, const char* path, size_t col_begin, size_t col_end,
+                                           void* stream, dgq_layer** out);
 void dgq_layer_destroy(dgq_layer* layer);
 dgq_status dgq_layer_get_info(const dgq_layer* layer, dgq_layer_info* info);
 

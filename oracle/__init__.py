@@ -250,6 +250,17 @@ class _Backend:
                                              _p(ce), _p(ca), _p(ev)))
         return s1, s2, codes, ce, ca, int(ev[0])
 
+    @staticmethod
+    def dgq_to_bytes_unchecked(L: Layer) -> bytes:
+        """DGQ1 serialisation (proj/include/dgq/format.hpp:6-21) WITHOUT the
+        reference's validation — for corrupted-artifact fixtures."""
+        import struct
+
+        head = b"DGQ1" + struct.pack("<QQQB", L.h, L.o, L.g, L.mode)
+        return (head + np.ascontiguousarray(L.codes, np.uint8).tobytes() + np.ascontiguousarray(L.s2, np.int8).tobytes()
+                + np.ascontiguousarray(L.zp, np.uint8).tobytes() + np.ascontiguousarray(L.s1, "<f4").tobytes()
+                + np.ascontiguousarray(L.k, "<f4").tobytes() + np.float32(L.act_scale).astype("<f4").tobytes())
+
     def dgq_to_bytes(self, L: Layer) -> bytes:
         assert self.pfx == "ref_"
         n = C.c_size_t()

@@ -6,7 +6,7 @@ Public surface mirrors the reference's operator API (proj/include/dgq):
 plus the device-resident prepared layer `CudaLayer` (C ABI: include/dgq_b200.h)
 and the column-parallel multi-GPU wrapper in `parallel`.
 """
-from ._lib import (DgqError, FormatError, InvalidArgument, OverflowRuntimeError,  # noqa: F401
+from ._lib import (DgqError, FormatError, InvalidArgument, IoError, OverflowRuntimeError,  # noqa: F401
                    ValidationError, lib)
 from .api import (ActQuant, CudaLayer, DgqLayer, ForwardResult, IntGemmResult, calibrate, clip_interval,  # noqa: F401
                   dequantize_to_f32, dequantize_to_s8, dgq_forward, epilogue, fp16_round, host_forward,
@@ -19,5 +19,5 @@ __all__ = [
     "dequantize_to_f32",
     "dequantize_to_s8", "dgq_forward", "epilogue", "fp16_round", "int8_gemm", "layer_from_bytes",
     "quantize_activations", "validate_layer", "segmented_gemm_reference", "host_forward", "linear_multi", "gen_synthetic", "pack_u4", "random_layer", "unpack_u4",
-    "DgqError", "FormatError", "InvalidArgument", "OverflowRuntimeError", "ValidationError", "lib",
+    "DgqError", "FormatError", "InvalidArgument", "IoError", "OverflowRuntimeError", "ValidationError", "lib",
 ]

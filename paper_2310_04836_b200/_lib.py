@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("DGQ_B200_LIB") or os.path.join(_PKG, "libdgq_b200.so"
 
 _vp, _sz, _i, _f = C.c_void_p, C.c_size_t, C.c_int, C.c_float
 
-DGQ_OK, DGQ_EINVAL, DGQ_EVALIDATION, DGQ_EOVERFLOW, DGQ_ECUDA, DGQ_ENOMEM, DGQ_EFORMAT = range(7)
+DGQ_OK, DGQ_EINVAL, DGQ_EVALIDATION, DGQ_EOVERFLOW, DGQ_ECUDA, DGQ_ENOMEM, DGQ_EFORMAT, DGQ_EIO = range(8)
 MODE_STATIC, MODE_DYNAMIC = 0, 1
 OUT_F32, OUT_F16 = 0, 1
 
@@ -43,6 +43,10 @@ class FormatError(DgqError, ValueError):
         self.kind = kind
 
 
+class IoError(DgqError, OSError):
+    """dgq::io_error (proj/include/dgq/error.hpp:9)."""
+
+
 class InvalidArgument(DgqError, ValueError):
     """std::invalid_argument."""
 
@@ -66,6 +70,7 @@ _SIGS = {
     "dgq_layer_create": (_i, [_i, _sz, _sz, _sz, _i, _f, _vp, _vp, _vp, _vp, _vp, _sz, _sz, _i, _vp,
                               C.POINTER(_vp)]),
     "dgq_layer_create_from_dgq1": (_i, [_i, _vp, _sz, _sz, _sz, _vp, C.POINTER(_vp)]),
+    "dgq_layer_create_from_dgq1_file": (_i, [_i, C.c_char_p, _sz, _sz, _vp, C.POINTER(_vp)]),
     "dgq_layer_destroy": (None, [_vp]),
     "dgq_layer_get_info": (_i, [_vp, C.POINTER(LayerInfo)]),
     "dgq_linear_workspace_bytes": (_sz, [_vp, _sz]),
@@ -138,6 +143,8 @@ def check(status: int):
     field = (L.dgq_last_error_field() or b"").decode(errors="replace")
     if status == DGQ_EVALIDATION:
         raise ValidationError(status, msg, field)
+    if status == DGQ_EIO:
+        raise IoError(status, msg)
     if status == DGQ_EFORMAT:
         raise FormatError(status, msg, field)
     if status == DGQ_EINVAL:

@@ -174,6 +174,18 @@ class CudaLayer:
                                                    _stream(dev), C.byref(h)))
         return cls(device=dev, _handle=h)
 
+    @classmethod
+    def from_dgq1_file(cls, path: str, device=None, col_begin: int = 0, col_end: int | None = None) -> "CudaLayer":
+        """A DGQ1 file streamed to the device (dgq_layer_create_from_dgq1_file):
+        code rows in ~32 MB slabs, validated on the GPU, only the shard's
+        columns uploaded."""
+        dev = _device_index(device)
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            check(lib().dgq_layer_create_from_dgq1_file(dev, str(path).encode(), int(col_begin), int(col_end or 0),
+                                                        _stream(dev), C.byref(h)))
+        return cls(device=dev, _handle=h)
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             lib().dgq_layer_destroy(self._h)

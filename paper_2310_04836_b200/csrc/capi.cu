@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -338,21 +339,78 @@ void dgq_layer_destroy(dgq_layer* L) {
   delete L;
 }
 
-dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, float act_scale,
-                            const uint8_t* codes, const int8_t* s2, const uint8_t* zp, const float* s1,
-                            const float* k, size_t col_begin, size_t col_end, int validate, void* stream,
-                            dgq_layer** out) {
+// validate_layer's O(h + o) checks (proj/src/format.cpp:48-59), in the
+// reference's order; the O(h o) ones run on the GPU (create_layer).
+static dgq_status validate_scalars(size_t h, size_t o, int mode, float act_scale, const float* s1, const float* k,
+                                   std::string* field, std::string* msg) {
+  for (size_t c = 0; c < o; ++c)
+    if (!(s1[c] > 0.0f) || !std::isfinite(s1[c])) {
+      *field = "s1";
+      *msg = "scales must be positive and finite";
+      return DGQ_EVALIDATION;
+    }
+  for (size_t j = 0; j < h; ++j)
+    if (!(k[j] >= 1.0f) || !std::isfinite(k[j])) {
+      *field = "k";
+      *msg = "smoothing scales must be >= 1";
+      return DGQ_EVALIDATION;
+    }
+  if (mode == DGQ_MODE_STATIC && !(act_scale > 0.0f)) {
+    *field = "act_scale";
+    *msg = "static mode requires a positive activation scale";
+    return DGQ_EVALIDATION;
+  }
+  if (!(act_scale >= 0.0f) || !std::isfinite(act_scale)) {
+    *field = "act_scale";
+    *msg = "must be finite and non-negative";
+    return DGQ_EVALIDATION;
+  }
+  return DGQ_OK;
+}
+
+// Source of the packed code rows (reference layout, o/2 bytes per row):
+// returns a host pointer to rows [r0, r0 + rows) (row pitch o/2), valid until
+// the next call with the same buffer index.
+using RowFetch = std::function<const uint8_t*(size_t r0, size_t rows, int buf)>;
+
+// The prepared layer.  Fused group sizes take the streaming path: the shard's
+// S2 / ZP columns are uploaded once, the codes in k-block-aligned slabs of
+// ~32 MB (only the shard's columns), each slab validated on the GPU (S2 range
+// and clip intervals, first violation in the reference's loop order) and
+// repacked into its k-blocks, so neither host nor device ever holds a second
+// full copy of the weights.  validate != 0 reports failures exactly as
+// dgq::validate_layer (proj/src/format.cpp:24-75) would, restricted to the
+// shard's columns for S2 and codes.
+static dgq_status create_layer(int device, size_t h, size_t o, size_t g, int mode, float act_scale,
+                               const RowFetch& fetch, const uint8_t* codes_full, const int8_t* s2, const uint8_t* zp,
+                               const float* s1, const float* k, size_t col_begin, size_t col_end, int validate,
+                               void* stream, dgq_layer** out, cudaEvent_t* copy_done = nullptr) {
   if (!out) return fail(DGQ_EINVAL, "out is null");
   *out = nullptr;
+  auto bad = [](const std::string& field, const std::string& m) {
+    return fail(DGQ_EVALIDATION, "invalid DgqLayer field '" + field + "': " + m, field);
+  };
   if (validate) {
-    dgq_status st = dgq_validate_layer(h, o, g, mode, act_scale, codes, s2, zp, s1, k);
-    if (st != DGQ_OK) return st;
+    if (h == 0 || o == 0) return bad("shape", "h and o must be positive");
+    if (o % 2) return bad("shape", "o must be even for packed 4-bit storage");
+    if (g == 0 || h % g) return bad("g", "group size must divide h");
   } else if (h == 0 || o == 0 || o % 2 || g == 0 || h % g) {
     return fail(DGQ_EINVAL, "inconsistent layer shape");
   }
+  if (!s2 || !zp || !s1 || !k) return fail(DGQ_EINVAL, "null layer array");
   if (col_end == 0) col_end = o;
   if (col_begin >= col_end || col_end > o) return fail(DGQ_EINVAL, "bad column shard range");
+  if (col_begin % 2 || col_end % 2) return fail(DGQ_EINVAL, "column shard bounds must be even (packed 4-bit storage)");
   if (h > (1u << 30) || o > (1u << 30)) return fail(DGQ_EINVAL, "layer too large");
+  const bool fused = dgq_layout::fused_ok(static_cast<int>(g));
+  if (!fused) {
+    // exotic group sizes keep the host validation and a full upload (below)
+    if (!codes_full) return fail(DGQ_EINVAL, "this group size needs the codes in memory");
+    if (validate) {
+      dgq_status st = dgq_validate_layer(h, o, g, mode, act_scale, codes_full, s2, zp, s1, k);
+      if (st != DGQ_OK) return st;
+    }
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int prev_dev = 0;
   DGQ_CUDA(cudaGetDevice(&prev_dev));
@@ -375,16 +433,17 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
   L->n_pad = round_up(L->o, 128);
   L->n_tiles = static_cast<int>(L->n_pad / 128);
   L->k_blocks = static_cast<int>(L->k_pad / 128);
-  L->fused = dgq_layout::fused_ok(static_cast<int>(g));
+  L->fused = fused;
 
-  const size_t ng = h / g;
-  const size_t codes_b = h * o / 2, s2_b = ng * o, zp_b = ng * o / 2;
+  const size_t ng = h / g, w = L->o, c0 = col_begin;
   uint8_t *d_codes = nullptr, *d_zp = nullptr;
   int8_t* d_s2 = nullptr;
+  unsigned long long* d_first = nullptr;
   auto cleanup_tmp = [&] {
     cudaFree(d_codes);
     cudaFree(d_s2);
     cudaFree(d_zp);
+    cudaFree(d_first);
   };
 #define DGQ_CUDA_L(expr)                        \
   do {                                          \
@@ -396,12 +455,6 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
                   std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     }                                           \
   } while (0)
-  DGQ_CUDA_L(cudaMalloc(&d_codes, codes_b));
-  DGQ_CUDA_L(cudaMalloc(&d_s2, s2_b));
-  DGQ_CUDA_L(cudaMalloc(&d_zp, zp_b));
-  DGQ_CUDA_L(cudaMemcpyAsync(d_codes, codes, codes_b, cudaMemcpyHostToDevice, st));
-  DGQ_CUDA_L(cudaMemcpyAsync(d_s2, s2, s2_b, cudaMemcpyHostToDevice, st));
-  DGQ_CUDA_L(cudaMemcpyAsync(d_zp, zp, zp_b, cudaMemcpyHostToDevice, st));
   DGQ_CUDA_L(cudaMalloc(&L->s1, L->o * sizeof(float)));
   DGQ_CUDA_L(cudaMalloc(&L->k, h * sizeof(float)));
   DGQ_CUDA_L(cudaMemcpyAsync(L->s1, s1 + col_begin, L->o * sizeof(float), cudaMemcpyHostToDevice, st));
@@ -427,15 +480,85 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
     }
   }
   L->device_bytes = (L->o + h) * sizeof(float);
-  if (L->fused) {
+  if (fused) {
     const size_t tb = static_cast<size_t>(L->n_tiles) * L->k_blocks * dgq_layout::chunk_bytes(static_cast<int>(g));
     DGQ_CUDA_L(cudaMalloc(&L->tiles, tb));
     L->device_bytes += tb;
-    DGQ_CUDA_L(dgq_launch_repack(d_codes, d_s2, d_zp, static_cast<int>(h), static_cast<int>(o), static_cast<int>(g),
-                                 static_cast<int>(col_begin), static_cast<int>(L->o), L->n_tiles, L->k_blocks,
-                                 L->tiles, st));
+    // the shard's S2 / ZP columns, dense [n_g x w] / [n_g x w/2]
+    DGQ_CUDA_L(cudaMalloc(&d_s2, ng * w));
+    DGQ_CUDA_L(cudaMalloc(&d_zp, ng * w / 2));
+    DGQ_CUDA_L(cudaMemcpy2DAsync(d_s2, w, s2 + c0, o, w, ng, cudaMemcpyHostToDevice, st));
+    DGQ_CUDA_L(cudaMemcpy2DAsync(d_zp, w / 2, zp + c0 / 2, o / 2, w / 2, ng, cudaMemcpyHostToDevice, st));
+    DGQ_CUDA_L(cudaMalloc(&d_first, 2 * sizeof(unsigned long long)));
+    DGQ_CUDA_L(cudaMemsetAsync(d_first, 0xFF, 2 * sizeof(unsigned long long), st));
+    // slabs: k-block and group aligned, ~32 MB of the shard's codes
+    const size_t unit = g > 128 ? g : 128;
+    size_t rows = std::max(unit, ((32u << 20) / std::max<size_t>(w / 2, 1)) / unit * unit);
+    if (rows > h) rows = round_up(h, unit);
+    DGQ_CUDA_L(cudaMalloc(&d_codes, rows * (w / 2)));
+    int buf = 0;
+    for (size_t r0 = 0; r0 < h; r0 += rows, buf ^= 1) {
+      const size_t n = std::min(rows, h - r0);
+      const uint8_t* src = fetch(r0, n, buf);
+      if (!src) {
+        cleanup_tmp();
+        dgq_layer_destroy(L);
+        return fail(DGQ_EFORMAT, "could not read the code rows of the artifact", "truncated");
+      }
+      DGQ_CUDA_L(cudaMemcpy2DAsync(d_codes, w / 2, src + c0 / 2, o / 2, w / 2, n, cudaMemcpyHostToDevice, st));
+      if (copy_done) DGQ_CUDA_L(cudaEventRecord(copy_done[buf], st));  // the host buffer may be refilled after this
+      if (validate)
+        DGQ_CUDA_L(dgq_launch_validate(d_codes, d_s2, d_zp, static_cast<int>(r0), static_cast<int>(n),
+                                       static_cast<int>(g), static_cast<int>(ng), static_cast<int>(w),
+                                       static_cast<int>(c0), static_cast<int>(o), r0 == 0 ? d_first : nullptr,
+                                       d_first + 1, st));
+      DGQ_CUDA_L(dgq_launch_repack_slab(d_codes, d_s2, d_zp, static_cast<int>(h), static_cast<int>(r0),
+                                        static_cast<int>(n), static_cast<int>(g), static_cast<int>(w), L->n_tiles,
+                                        L->k_blocks, L->tiles, st));
+    }
+    if (validate) {
+      unsigned long long first[2];
+      DGQ_CUDA_L(cudaMemcpyAsync(first, d_first, sizeof first, cudaMemcpyDeviceToHost, st));
+      DGQ_CUDA_L(cudaStreamSynchronize(st));
+      std::string field, msg;
+      dgq_status vs = DGQ_OK;
+      if (first[0] != ~0ull) {  // S2 outside [1, 127] (proj/src/format.cpp:44-47)
+        const size_t kg = first[0] / o, c = first[0] % o;
+        int8_t v = 0;
+        std::memcpy(&v, s2 + kg * o + c, 1);
+        field = "s2";
+        msg = "value " + std::to_string(int(v)) + " outside [1, 127]";
+        vs = DGQ_EVALIDATION;
+      } else {
+        vs = validate_scalars(h, o, mode, act_scale, s1, k, &field, &msg);
+        if (vs == DGQ_OK && first[1] != ~0ull) {  // clip intervals (proj/src/format.cpp:60-74)
+          const size_t j = first[1] % g, kc = first[1] / g, kg = kc / o, c = kc % o, i = kg * g + j;
+          const int sv = s2[kg * o + c], z = nib(zp, kg * o + c), q = 127 / sv;
+          const int lo = std::max(0, z - q), hi = std::min(15, z + q);
+          int code = -1;
+          const uint8_t* row = fetch(i, 1, 0);
+          if (row) code = nib(row, c);
+          field = "codes";
+          msg = "code " + std::to_string(code) + " at (" + std::to_string(i) + ", " + std::to_string(c) +
+                ") outside clip interval [" + std::to_string(lo) + ", " + std::to_string(hi) + "]";
+          vs = DGQ_EVALIDATION;
+        }
+      }
+      if (vs != DGQ_OK) {
+        cleanup_tmp();
+        dgq_layer_destroy(L);
+        return bad(field, msg);
+      }
+    }
   } else {
     // exotic group sizes: materialise W_s8 once, transpose to K-major
+    const size_t codes_b = h * o / 2, s2_b = ng * o, zp_b = ng * o / 2;
+    DGQ_CUDA_L(cudaMalloc(&d_codes, codes_b));
+    DGQ_CUDA_L(cudaMalloc(&d_s2, s2_b));
+    DGQ_CUDA_L(cudaMalloc(&d_zp, zp_b));
+    DGQ_CUDA_L(cudaMemcpyAsync(d_codes, codes_full, codes_b, cudaMemcpyHostToDevice, st));
+    DGQ_CUDA_L(cudaMemcpyAsync(d_s2, s2, s2_b, cudaMemcpyHostToDevice, st));
+    DGQ_CUDA_L(cudaMemcpyAsync(d_zp, zp, zp_b, cudaMemcpyHostToDevice, st));
     int8_t* w_full = nullptr;
     unsigned long long* d_bad = nullptr;
     DGQ_CUDA_L(cudaMalloc(&w_full, h * o));
@@ -471,6 +594,17 @@ dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, 
   return DGQ_OK;
 }
 
+dgq_status dgq_layer_create(int device, size_t h, size_t o, size_t g, int mode, float act_scale,
+                            const uint8_t* codes, const int8_t* s2, const uint8_t* zp, const float* s1,
+                            const float* k, size_t col_begin, size_t col_end, int validate, void* stream,
+                            dgq_layer** out) {
+  if (!codes) return fail(DGQ_EINVAL, "null layer array");
+  const size_t pitch = o / 2;
+  RowFetch fetch = [codes, pitch](size_t r0, size_t, int) { return codes + r0 * pitch; };
+  return create_layer(device, h, o, g, mode, act_scale, fetch, codes, s2, zp, s1, k, col_begin, col_end, validate,
+                      stream, out);
+}
+
 dgq_status dgq_layer_create_from_dgq1(int device, const uint8_t* bytes, size_t nbytes, size_t col_begin,
                                       size_t col_end, void* stream, dgq_layer** out) {
   // DGQ1 layout, proj/include/dgq/format.hpp:6-21; checks of proj/src/format.cpp:214-250
@@ -490,7 +624,10 @@ dgq_status dgq_layer_create_from_dgq1(int device, const uint8_t* bytes, size_t n
   if (h > (1ull << 30) || o > (1ull << 30)) return fail(DGQ_EFORMAT, "dimensions too large", "bad_header");
   const uint64_t ng = h / g;
   const uint64_t need = kHeader + h * o / 2 + ng * o + ng * o / 2 + 4 * o + 4 * h + 4;
-  if (nbytes < need) return fail(DGQ_EFORMAT, "truncated payload", "truncated");
+  if (nbytes < need)
+    return fail(DGQ_EFORMAT,
+                "truncated payload: have " + std::to_string(nbytes) + " bytes, header implies " + std::to_string(need),
+                "truncated");
   if (nbytes > need) return fail(DGQ_EFORMAT, "payload longer than the header implies", "size_mismatch");
   const uint8_t* p = bytes + kHeader;
   const uint8_t* codes = p;
@@ -508,6 +645,101 @@ dgq_status dgq_layer_create_from_dgq1(int device, const uint8_t* bytes, size_t n
   std::memcpy(&act_scale, p, 4);
   return dgq_layer_create(device, h, o, g, mode, act_scale, codes, s2, zp, s1.data(), k.data(), col_begin, col_end,
                           1, stream, out);
+}
+
+// DGQ1 file -> prepared (sharded) layer without holding the artifact in host
+// memory: header, S2 / ZP / s1 / k / act_scale are read first (small), then the
+// code rows stream through two pinned slabs into the GPU validator + repack.
+dgq_status dgq_layer_create_from_dgq1_file(int device, const char* path, size_t col_begin, size_t col_end,
+                                           void* stream, dgq_layer** out) {
+  constexpr size_t kHeader = 29;
+  if (!path || !out) return fail(DGQ_EINVAL, "null argument");
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(DGQ_EIO, std::string("cannot open: ") + path, "io");  // read_dgq, proj/src/format.cpp:276-278
+  struct Closer {
+    std::FILE* f;
+    ~Closer() { std::fclose(f); }
+  } closer{f};
+  fseeko(f, 0, SEEK_END);
+  const long long nbytes = static_cast<long long>(ftello(f));
+  fseeko(f, 0, SEEK_SET);
+  uint8_t hdr[kHeader];
+  if (nbytes < static_cast<long long>(kHeader) || std::fread(hdr, 1, kHeader, f) != kHeader)
+    return fail(DGQ_EFORMAT, "truncated: DGQ file shorter than the header", "truncated");
+  if (std::memcmp(hdr, "DGQ1", 4) != 0) return fail(DGQ_EFORMAT, "bad magic, expected \"DGQ1\"", "bad_magic");
+  auto u64 = [&](size_t off) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(hdr[off + i]) << (8 * i);
+    return v;
+  };
+  const uint64_t h = u64(4), o = u64(12), g = u64(20);
+  const uint8_t mode = hdr[28];
+  if (mode > 1) return fail(DGQ_EFORMAT, "unknown mode byte " + std::to_string(int(mode)), "bad_header");
+  if (h == 0 || o == 0 || o % 2 || g == 0 || h % g)
+    return fail(DGQ_EFORMAT, "inconsistent dimensions in header", "bad_header");
+  if (h > (1ull << 30) || o > (1ull << 30)) return fail(DGQ_EFORMAT, "dimensions too large", "bad_header");
+  const uint64_t ng = h / g;
+  const uint64_t need = kHeader + h * o / 2 + ng * o + ng * o / 2 + 4 * o + 4 * h + 4;
+  if (static_cast<uint64_t>(nbytes) < need)
+    return fail(DGQ_EFORMAT,
+                "truncated payload: have " + std::to_string(nbytes) + " bytes, header implies " + std::to_string(need),
+                "truncated");
+  if (static_cast<uint64_t>(nbytes) > need)
+    return fail(DGQ_EFORMAT, "payload longer than the header implies", "size_mismatch");
+  const long long off_s2 = kHeader + h * o / 2;
+  std::vector<int8_t> s2(ng * o);
+  std::vector<uint8_t> zp(ng * o / 2);
+  std::vector<float> s1(o), k(h);
+  float act_scale = 0.0f;
+  fseeko(f, static_cast<off_t>(off_s2), SEEK_SET);
+  if (std::fread(s2.data(), 1, s2.size(), f) != s2.size() || std::fread(zp.data(), 1, zp.size(), f) != zp.size() ||
+      std::fread(s1.data(), 4, o, f) != o || std::fread(k.data(), 4, h, f) != h ||
+      std::fread(&act_scale, 4, 1, f) != 1)
+    return fail(DGQ_EIO, std::string("read failed: ") + path, "io");
+  // two pinned row slabs (the loader's slab is <= 32 MB of the shard; full rows are read)
+  const size_t pitch = o / 2;
+  uint8_t* pinned[2] = {nullptr, nullptr};
+  size_t cap = 0;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int prev_dev = 0;
+  DGQ_CUDA(cudaGetDevice(&prev_dev));
+  DGQ_CUDA(cudaSetDevice(device));
+  for (auto& e : done) DGQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaSetDevice(prev_dev);
+  bool used[2] = {false, false};
+  RowFetch fetch = [&](size_t r0, size_t rows, int b) -> const uint8_t* {
+    const size_t bytes = rows * pitch;
+    if (used[b]) cudaEventSynchronize(done[b]);  // the previous copy out of this slab finished
+    if (bytes > cap) {
+      for (auto& p : pinned) {
+        cudaFreeHost(p);
+        p = nullptr;
+      }
+      if (cudaHostAlloc(&pinned[0], bytes, cudaHostAllocDefault) != cudaSuccess ||
+          cudaHostAlloc(&pinned[1], bytes, cudaHostAllocDefault) != cudaSuccess)
+        return nullptr;
+      cap = bytes;
+    }
+    fseeko(f, static_cast<off_t>(kHeader + r0 * pitch), SEEK_SET);
+    if (std::fread(pinned[b], 1, bytes, f) != bytes) return nullptr;
+    used[b] = true;
+    return pinned[b];
+  };
+  dgq_status st = create_layer(device, h, o, g, mode, act_scale, fetch, nullptr, s2.data(), zp.data(), s1.data(),
+                               k.data(), col_begin, col_end, 1, stream, out, done);
+  if (st == DGQ_EINVAL && !dgq_layout::fused_ok(static_cast<int>(g))) {
+    // exotic group sizes need the codes in memory: read them whole
+    std::vector<uint8_t> codes(h * o / 2);
+    fseeko(f, static_cast<off_t>(kHeader), SEEK_SET);
+    if (std::fread(codes.data(), 1, codes.size(), f) != codes.size())
+      st = fail(DGQ_EIO, std::string("read failed: ") + path, "io");
+    else
+      st = dgq_layer_create(device, h, o, g, mode, act_scale, codes.data(), s2.data(), zp.data(), s1.data(),
+                            k.data(), col_begin, col_end, 1, stream, out);
+  }
+  for (auto& p : pinned) cudaFreeHost(p);
+  for (auto& e : done) cudaEventDestroy(e);
+  return st;
 }
 
 dgq_status dgq_layer_get_info(const dgq_layer* L, dgq_layer_info* info) {

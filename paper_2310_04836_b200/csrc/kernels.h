@@ -180,6 +180,15 @@ inline cudaError_t dgq_allow_smem(F* kernel, size_t bytes) {
 // slice [c0, c0+n) -> prepared tiles.
 cudaError_t dgq_launch_repack(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int h, int o_full, int g,
                               int c0, int n, int n_tiles, int k_blocks, uint8_t* tiles, cudaStream_t st);
+// streaming loader: rows [r0, r0 + rows) (k-block aligned r0) of a shard's codes
+// (dense [rows x n/2]) with the shard's full S2 / ZP ([n_g x n]) -> those k-blocks
+cudaError_t dgq_launch_repack_slab(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int h, int r0, int rows,
+                                   int g, int n, int n_tiles, int k_blocks, uint8_t* tiles, cudaStream_t st);
+// validate_layer's S2 range (first_s2 may be null) and clip-interval checks on
+// a shard / slab, first violation in the reference's loop order (atomicMin keys)
+cudaError_t dgq_launch_validate(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int r0, int rows, int g,
+                                int n_g, int n, int c0, int o_full, unsigned long long* first_s2,
+                                unsigned long long* first_code, cudaStream_t st);
 // prepared tiles -> W_s8 row-major [h x n] (same dequantiser as the fused GEMM)
 cudaError_t dgq_launch_dequant_tiles(const uint8_t* tiles, int g, int h, int n, int n_tiles, int k_blocks,
                                      int8_t* w, size_t ldw, cudaStream_t st);

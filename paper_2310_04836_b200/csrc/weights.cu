@@ -63,6 +63,81 @@ __global__ void k_repack(const uint8_t* __restrict__ codes, const int8_t* __rest
   }
 }
 
+// Slab form of the repack for the streaming loader: rows [r0, r0 + rows) of
+// the shard's codes (dense [rows x n_cols/2], k-block aligned r0) plus the
+// shard's full S2 / ZP ([n_g x n_cols]) -> k-blocks [r0/128, ...) of the tiles.
+__global__ void k_repack_slab(const uint8_t* __restrict__ codes, const int8_t* __restrict__ s2,
+                              const uint8_t* __restrict__ zp, int h, int r0, int rows, int g, int n_cols, int n_tiles,
+                              int k_blocks, int chunk_bytes, int gpk, uint8_t* __restrict__ tiles) {
+  const int kb_slab = (rows + 127) / 128, kb0 = r0 / 128;
+  const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const size_t total = static_cast<size_t>(n_tiles) * kb_slab * 4 * 128;
+  if (tid >= total) return;
+  const int n = static_cast<int>(tid % 128);
+  const int j = static_cast<int>((tid / 128) % 4);
+  const size_t b = tid / 512;
+  const int kb = kb0 + static_cast<int>(b % kb_slab);
+  const int nt = static_cast<int>(b / kb_slab);
+  const int col = nt * 128 + n;
+  const bool cvalid = col < n_cols;
+  uint8_t* chunk = tiles + (static_cast<size_t>(nt) * k_blocks + kb) * static_cast<size_t>(chunk_bytes);
+  uint32_t words[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int k = kb * 128 + j * 32 + w * 8 + t;  // global row
+      uint32_t c = 0;
+      if (cvalid && k < h) c = ref_nibble(codes, static_cast<size_t>(k - r0) * n_cols + col);
+      word |= c << (4 * c_nib_pos[t]);
+    }
+    words[w] = word;
+  }
+  *reinterpret_cast<uint4*>(chunk + j * 2048 + n * 16) = make_uint4(words[0], words[1], words[2], words[3]);
+  if (j == 0) {
+    uint16_t* sc = reinterpret_cast<uint16_t*>(chunk + 8192);
+    for (int gi = 0; gi < gpk; ++gi) {
+      const int kstart = kb * 128 + (g >= 128 ? 0 : gi * g);
+      uint32_t sv = 1u;  // S2 = 1, ZP = 0 for padding
+      if (cvalid && kstart < h) {
+        const size_t grp = static_cast<size_t>(kstart / g);
+        sv = static_cast<uint32_t>(static_cast<uint8_t>(s2[grp * n_cols + col])) |
+             (ref_nibble(zp, grp * n_cols + col) << 8);
+      }
+      sc[gi * 128 + n] = static_cast<uint16_t>(sv);
+    }
+  }
+}
+
+// validate_layer's O(h o) checks on the GPU (proj/src/format.cpp:44-47, 60-74),
+// over a column shard [c0, c0 + n_cols) of an o_full-wide layer.  The first
+// violation in the reference's loop order wins: S2 by flat (group, column)
+// index, codes by (group, column, row within the group).  ~0 = none.
+__global__ void k_validate_s2(const int8_t* __restrict__ s2, int n_g, int n_cols, int c0, int o_full,
+                              unsigned long long* first) {
+  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<size_t>(n_g) * n_cols) return;
+  const size_t kg = idx / n_cols, c = idx % n_cols;
+  if (s2[idx] < 1) atomicMin(first, static_cast<unsigned long long>(kg * o_full + c0 + c));
+}
+__global__ void k_validate_codes(const uint8_t* __restrict__ codes, const int8_t* __restrict__ s2,
+                                 const uint8_t* __restrict__ zp, int r0, int rows, int g, int n_cols, int c0,
+                                 int o_full, unsigned long long* first) {
+  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<size_t>(rows) * n_cols) return;
+  const size_t il = idx / n_cols, c = idx % n_cols;
+  const size_t i = r0 + il, kg = i / g;
+  const int sv = s2[kg * n_cols + c];
+  if (sv < 1) return;  // reported by k_validate_s2 first
+  const int z = static_cast<int>(ref_nibble(zp, kg * n_cols + c));
+  const int q = 127 / sv;
+  const int lo = z - q > 0 ? z - q : 0, hi = z + q < 15 ? z + q : 15;
+  const int code = static_cast<int>(ref_nibble(codes, idx));
+  if (code < lo || code > hi)
+    atomicMin(first, static_cast<unsigned long long>((kg * o_full + c0 + c) * g + (i - kg * g)));
+}
+
 // prepared tiles -> row-major W_s8 via the fused kernel's dequantiser
 __global__ void k_dequant_tiles(const uint8_t* __restrict__ tiles, int chunk_bytes, int gshift, int h, int n_cols,
                                 int n_tiles, int k_blocks, int8_t* __restrict__ w, size_t ldw) {
@@ -137,6 +212,30 @@ cudaError_t dgq_launch_repack(const uint8_t* codes, const int8_t* s2, const uint
   const int cb = dgq_layout::chunk_bytes(g), gpk = dgq_layout::groups_per_kblock(g);
   k_repack<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(codes, s2, zp, h, o_full, g, c0, n, n_tiles,
                                                                         k_blocks, cb, gpk, tiles);
+  return cudaGetLastError();
+}
+
+cudaError_t dgq_launch_repack_slab(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int h, int r0, int rows,
+                                   int g, int n_cols, int n_tiles, int k_blocks, uint8_t* tiles, cudaStream_t st) {
+  const size_t total = static_cast<size_t>(n_tiles) * ((rows + 127) / 128) * 512;
+  if (!total) return cudaSuccess;
+  const int cb = dgq_layout::chunk_bytes(g), gpk = dgq_layout::groups_per_kblock(g);
+  k_repack_slab<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(codes, s2, zp, h, r0, rows, g, n_cols,
+                                                                             n_tiles, k_blocks, cb, gpk, tiles);
+  return cudaGetLastError();
+}
+
+cudaError_t dgq_launch_validate(const uint8_t* codes, const int8_t* s2, const uint8_t* zp, int r0, int rows, int g,
+                                int n_g, int n_cols, int c0, int o_full, unsigned long long* first_s2,
+                                unsigned long long* first_code, cudaStream_t st) {
+  if (first_s2) {
+    const size_t n = static_cast<size_t>(n_g) * n_cols;
+    if (n) k_validate_s2<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(s2, n_g, n_cols, c0, o_full, first_s2);
+  }
+  const size_t n = static_cast<size_t>(rows) * n_cols;
+  if (n)
+    k_validate_codes<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(codes, s2, zp, r0, rows, g, n_cols, c0,
+                                                                              o_full, first_code);
   return cudaGetLastError();
 }
 

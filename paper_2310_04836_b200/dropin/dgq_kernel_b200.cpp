@@ -50,6 +50,8 @@ void check(dgq_status st) {
       throw validation_error(dgq_last_error_field(), msg);
     case DGQ_EFORMAT:
       throw format_error(format_kind(dgq_last_error_field()), msg);
+    case DGQ_EIO:
+      throw io_error(msg);
     default:
       throw std::runtime_error("dgq_b200: " + msg);
   }

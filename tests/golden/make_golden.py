@@ -116,6 +116,54 @@ def main():
     put("dgq1", bytes=np.frombuffer(R.dgq_to_bytes(L3), np.uint8), h=64, o=32, g=16, codes=L3.codes, s2=L3.s2,
         zp=L3.zp, s1=L3.s1, k=L3.k, act_scale=np.float32(0.05), mode=0)
 
+    # DGQ1 artifacts through the reference's forward (the device-loaded layer must
+    # reproduce w_s8 and the output), and corrupted artifacts with the
+    # reference's validate_layer verdict (first failure in its loop order)
+    X3 = R.gen_synthetic(9, 64, 44, 3, 50.0, 7)
+    out3, w3, *_ = R.dgq_forward(X3, L3, None, 0)
+    put("dgq1", w_s8=w3, X=X3, out=out3)
+    L4 = oracle.random_layer(512, 384, 128, seed=8, mode=1)
+    L4.k, _ = R.smooth_from_calib(R.gen_synthetic(64, 512, 9, 3, 50.0, 7), 0.005)
+    X4 = R.gen_synthetic(33, 512, 45, 3, 50.0, 7)
+    out4, w4, *_ = R.dgq_forward(X4, L4, None, 0)
+    put("dgq1b", bytes=np.frombuffer(R.dgq_to_bytes(L4), np.uint8), w_s8=w4, X=X4, out=out4)
+
+    def corrupt(name, L, edit):
+        C = oracle.Layer(h=L.h, o=L.o, g=L.g, codes=L.codes.copy(), s2=L.s2.copy(), zp=L.zp.copy(),
+                         s1=L.s1.copy(), k=L.k.copy(), act_scale=L.act_scale, mode=L.mode)
+        edit(C)
+        try:
+            R.validate_layer(C)
+            raise SystemExit(f"{name}: the reference accepted the corrupted layer")
+        except oracle.OracleError as e:
+            field, msg = e.field, str(e).split(": ", 1)[1]
+        put(name, bytes=np.frombuffer(R.dgq_to_bytes_unchecked(C), np.uint8), field=np.array(field),
+            msg=np.array(msg))
+
+    def set_code(C, i, c, v):
+        u = oracle.unpack_u4(C.codes, C.h * C.o)
+        u[i * C.o + c] = v
+        C.codes = oracle.pack_u4(u)
+
+    def bad_codes(C):  # two violations: the reference reports the first in (group, column, row) order
+        s2 = C.s2.reshape(-1, C.o)
+        s2[2, 7] = s2[1, 300] = 127  # clip interval collapses to {ZP}
+        zp = oracle.unpack_u4(C.zp, s2.size).reshape(s2.shape)
+        set_code(C, 2 * 128 + 5, 7, (int(zp[2, 7]) + 3) % 16)
+        set_code(C, 1 * 128 + 100, 300, (int(zp[1, 300]) + 5) % 16)
+
+    def bad_s2_and_codes(C):
+        bad_codes(C)
+        C.s2[3 * C.o + 11] = 0
+
+    def bad_s1_and_codes(C):
+        bad_codes(C)
+        C.s1[17] = -1.0
+
+    corrupt("dgq1_badcodes", L4, bad_codes)
+    corrupt("dgq1_bads2", L4, bad_s2_and_codes)
+    corrupt("dgq1_bads1", L4, bad_s1_and_codes)
+
     path = os.path.join(HERE, "golden_v1.npz")
     np.savez_compressed(path, **out)
     print(path, os.path.getsize(path), "bytes,", len(out), "arrays")

@@ -461,15 +461,49 @@ def test_column_shards_concatenate_to_full(cuda, port):
     assert np.array_equal(bits(np.concatenate(parts, axis=1)), bits(out))
 
 
-def test_dgq1_to_device_layer(cuda, golden, port):
-    raw = golden["dgq1.bytes"].tobytes()
-    CL = dgq.CudaLayer.from_dgq1(raw)
-    L = dgq.layer_from_bytes(raw)
-    assert (CL.h, CL.o) == (L.h, L.o)
-    assert np.array_equal(CL.dequant_s8().cpu().numpy(), golden["dgq1.w_s8"] if "dgq1.w_s8" in golden else
-                          dgq.dequantize_to_s8(L))
+@pytest.mark.parametrize("case", ["dgq1", "dgq1b"])
+def test_dgq1_to_device_layer(cuda, golden, case, tmp_path):
+    # DGQ1 artifact (proj/include/dgq/format.hpp:6-21) -> device layer, from bytes
+    # and streamed from a file, whole and as column shards: W_s8 and the forward
+    # output equal the reference's own dequantize_to_s8 / dgq_forward
+    raw = golden[f"{case}.bytes"].tobytes()
+    path = tmp_path / f"{case}.dgq"
+    path.write_bytes(raw)
+    w_ref, X, out = golden[f"{case}.w_s8"], golden[f"{case}.X"], golden[f"{case}.out"]
+    o = w_ref.shape[1]
+    x = torch.from_numpy(X).cuda()
+    for CL in (dgq.CudaLayer.from_dgq1(raw), dgq.CudaLayer.from_dgq1_file(path)):
+        assert np.array_equal(CL.dequant_s8().cpu().numpy(), w_ref)
+        assert np.array_equal(bits(CL.forward(x, out_dtype=torch.float32).cpu().numpy()), bits(out))
+    c0, c1 = (o // 4) & ~1, (3 * o // 4) & ~1
+    for S in (dgq.CudaLayer.from_dgq1(raw, col_begin=c0, col_end=c1),
+              dgq.CudaLayer.from_dgq1_file(path, col_begin=c0, col_end=c1)):
+        assert S.o == c1 - c0
+        assert np.array_equal(S.dequant_s8().cpu().numpy(), w_ref[:, c0:c1])
+        assert np.array_equal(bits(S.forward(x, out_dtype=torch.float32).cpu().numpy()), bits(out[:, c0:c1]))
     with pytest.raises(dgq.FormatError):
         dgq.CudaLayer.from_dgq1(raw[:-3])
+    (tmp_path / "short.dgq").write_bytes(raw[:-3])
+    with pytest.raises(dgq.FormatError, match="truncated"):
+        dgq.CudaLayer.from_dgq1_file(tmp_path / "short.dgq")
+    with pytest.raises(dgq.IoError, match="cannot open"):
+        dgq.CudaLayer.from_dgq1_file(tmp_path / "missing.dgq")
+
+
+@pytest.mark.parametrize("case", ["dgq1_badcodes", "dgq1_bads2", "dgq1_bads1"])
+def test_dgq1_gpu_validation_matches_reference(cuda, golden, case, tmp_path):
+    # the loader validates on the GPU (S2 range, clip intervals) in slabs; the
+    # first failure and its message equal the reference's validate_layer
+    # (proj/src/format.cpp:24-75) on the same corrupted artifact
+    raw = golden[f"{case}.bytes"].tobytes()
+    field, msg = str(golden[f"{case}.field"]), str(golden[f"{case}.msg"])
+    path = tmp_path / "bad.dgq"
+    path.write_bytes(raw)
+    for load in (lambda: dgq.CudaLayer.from_dgq1(raw), lambda: dgq.CudaLayer.from_dgq1_file(path)):
+        with pytest.raises(dgq.ValidationError) as ei:
+            load()
+        assert ei.value.field == field
+        assert str(ei.value).endswith(msg), (str(ei.value), msg)
 
 
 def test_max_accumulator_at_k28672(cuda):

@@ -20,7 +20,9 @@ ok = np.array_equal(y.cpu().numpy().view(np.uint32), out.view(np.uint32))
 print("case", M, h, o, g, mode, CL.plan(M), "bit-exact" if ok else "MISMATCH")
 PY
 for tool in memcheck racecheck synccheck; do
-  for c in "4 1024 512 128 1" "300 512 512 128 1025" "300 512 512 64 1" "64 512 256 128 1"; do
+  # K5d (forced, mode bit 27) | K5p S=1 | K5p S=2 (bit 30) | planner default (g=64) | one-CTA K5 | K1 v3 (M >= SMs)
+  for c in "4 4096 512 128 134217729" "300 512 512 128 1025" "600 1024 512 128 1073742849" "300 512 512 64 1" \
+           "64 512 256 128 1" "200 2048 256 128 1"; do
     echo "== $tool $c"
     timeout 600 compute-sanitizer --tool $tool --print-limit 5 python /tmp/san_case.py $c 2>&1 | grep -E "case|ERROR SUMMARY|Error|Hazard" | head -6
   done
