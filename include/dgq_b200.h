@@ -217,6 +217,22 @@ dgq_status dgq_phase2_search(const float* dW, size_t h, size_t o, const float* d
                              size_t n_alpha, float* dS1, int8_t* dS2, int32_t* dCodes, double* dColErr,
                              float* dColAlpha, uint64_t* evals, void* stream);
 
+/* ---- column-parallel linear + all-gather --------------------
+ * Rank r holds the column shard [r N/p, (r+1) N/p) of a layer
+ * (dgq_layer_create col_begin / col_end).  NCCL is resolved at run time
+ * (libnccl.so.2, preferring the copy already loaded in the process); `comm`
+ * is an ncclComm_t passed as void*, ours (dgq_comm_create) or the caller's. */
+#define DGQ_COMM_ID_BYTES 128
+dgq_status dgq_comm_unique_id(uint8_t* id /* [DGQ_COMM_ID_BYTES] */);
+dgq_status dgq_comm_create(int nranks, int rank, const uint8_t* id, int device, void** comm);
+void dgq_comm_destroy(void* comm);
+/* dgq_linear of this rank's shard into dY_local [M x o_shard] (dense), then an
+ * NCCL all-gather into dY_all [nranks][M][o_shard] on `stream`: the layout the
+ * next layer's K1 reads in place (dgq_quantize_act_f16, seg_cols = o_shard). */
+dgq_status dgq_linear_allgather(const dgq_layer* layer, const int8_t* dXq, size_t ldq, const float* dRowScale,
+                                size_t M, const float* dBias, int out_dtype, void* dY_local, void* dY_all, void* comm,
+                                void* stream);
+
 /* ---- measured dense INT8 tensor peak ----------------------------------------
  * The INT8 roofline denominator: every SM pair issues
  * tcgen05.mma.cta_group::2.kind::i8 (256 x 256 x 32, K5p's shape) back to back

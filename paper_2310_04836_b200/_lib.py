@@ -94,6 +94,10 @@ _SIGS = {
     "dgq_phase2_search": (_i, [_vp, _sz, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp,
                                C.POINTER(C.c_uint64), _vp]),
     "dgq_measure_i8_peak": (_i, [_i, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "dgq_comm_unique_id": (_i, [_vp]),
+    "dgq_comm_create": (_i, [_i, _i, _vp, _i, C.POINTER(_vp)]),
+    "dgq_comm_destroy": (None, [_vp]),
+    "dgq_linear_allgather": (_i, [_vp, _vp, _sz, _vp, _sz, _vp, _i, _vp, _vp, _vp, _vp]),
     # host-buffer API (the reference's calling convention)
     "dgq_host_quantize_activations": (_i, [_vp, _sz, _sz, _vp, _i, _f, _vp, _vp]),
     "dgq_host_dequantize_to_s8": (_i, [_sz, _sz, _sz, _vp, _vp, _vp, _vp]),

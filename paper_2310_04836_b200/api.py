@@ -72,8 +72,8 @@ class DgqLayer:
             np.float32(self.act_scale).tobytes()
 
 
-def validate_layer(layer: DgqLayer) -> None:
-    """proj/src/format.cpp:24-75; raises ValidationError(field)."""
+def _check_layer_arrays(layer: DgqLayer):
+    """The array-shape part of validate_layer (proj/src/format.cpp:31-42)."""
     codes, s2, zp, s1, k = layer.arrays()
     ng = layer.n_g
     if (layer.h and layer.o and layer.g and layer.o % 2 == 0 and layer.h % layer.g == 0 and
@@ -84,6 +84,13 @@ def validate_layer(layer: DgqLayer) -> None:
         raise ValidationError(_lib.DGQ_EVALIDATION, "invalid DgqLayer field 's1': expected length o", "s1")
     if k.size != layer.h and layer.h:
         raise ValidationError(_lib.DGQ_EVALIDATION, "invalid DgqLayer field 'k': expected length h", "k")
+    return codes, s2, zp, s1, k
+
+
+def validate_layer(layer: DgqLayer) -> None:
+    """proj/src/format.cpp:24-75; raises ValidationError(field).  (Host C-ABI
+    dgq_validate_layer; CudaLayer validates the same invariants on the GPU.)"""
+    codes, s2, zp, s1, k = _check_layer_arrays(layer)
     check(lib().dgq_validate_layer(layer.h, layer.o, layer.g, int(layer.mode), float(layer.act_scale),
                                    _np_ptr(codes), _np_ptr(s2), _np_ptr(zp), _np_ptr(s1), _np_ptr(k)))
 
@@ -150,9 +157,8 @@ class CudaLayer:
         if _handle is not None:
             self._h = _handle
         else:
-            codes, s2, zp, s1, k = layer.arrays()
-            if validate:
-                validate_layer(layer)
+            # array shapes here; the value invariants are checked on the GPU by dgq_layer_create
+            codes, s2, zp, s1, k = _check_layer_arrays(layer)
             with torch.cuda.device(self.device):
                 check(lib().dgq_layer_create(self.device, layer.h, layer.o, layer.g, int(layer.mode),
                                              float(layer.act_scale), _np_ptr(codes), _np_ptr(s2), _np_ptr(zp),

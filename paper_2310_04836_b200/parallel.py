@@ -52,14 +52,22 @@ def gathered_to_full(g):
 
 
 class ColumnParallelLinear:
-    """One DGQ linear, column-sharded over the ranks of `group`."""
+    """One DGQ linear, column-sharded over the ranks of `group`.
+
+    `shard_factory(layer, c0, c1)` builds the rank's shard (default: a CudaLayer
+    holding columns [c0, c1) on `device`); anything with the same
+    quantize_act / linear interface works, which is how the multi-process CPU
+    tests run this class over gloo with an oracle-backed shard."""
 
     def __init__(self, layer: DgqLayer, rank: int = 0, world: int = 1, device=None, group=None,
-                 validate: bool = True):
+                 validate: bool = True, shard_factory=None):
         self.rank, self.world, self.group = rank, world, group
         self.o_full = layer.o
         self.c0, self.c1 = shard_range(layer.o, rank, world)
-        self.layer = CudaLayer(layer, device=device, col_begin=self.c0, col_end=self.c1, validate=validate)
+        if shard_factory is None:
+            self.layer = CudaLayer(layer, device=device, col_begin=self.c0, col_end=self.c1, validate=validate)
+        else:
+            self.layer = shard_factory(layer, self.c0, self.c1)
         self.h = layer.h
         self.shard = self.c1 - self.c0
 
@@ -87,3 +95,57 @@ class ColumnParallelLinear:
 
     def close(self):
         self.layer.close()
+
+
+class DgqComm:
+    """The C-ABI communicator (dgq_comm_create over NCCL) for callers of
+    dgq_linear_allgather: rank 0 draws the unique id, torch.distributed (any
+    backend) broadcasts it; world 1 needs no process group."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device=None, group=None):
+        import ctypes as C
+
+        from ._lib import check, lib
+
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib().dgq_comm_unique_id(uid))
+        if world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        self.device = torch.cuda.current_device() if device is None else torch.device(device).index
+        self._h = C.c_void_p()
+        check(lib().dgq_comm_create(world, rank, uid, self.device, C.byref(self._h)))
+        self.world = world
+
+    def linear_allgather(self, lin: "ColumnParallelLinear", codes: torch.Tensor, rs: torch.Tensor,
+                         out_dtype=torch.float16, bias: torch.Tensor | None = None):
+        """dgq_linear_allgather: this rank's shard, then the [p][M][N/p] all-gather."""
+        import ctypes as C
+
+        from ._lib import OUT_F16, OUT_F32, check, lib
+
+        M = codes.shape[0]
+        local = torch.empty(M, lin.shard, dtype=out_dtype, device=codes.device)
+        full = torch.empty(self.world, M, lin.shard, dtype=out_dtype, device=codes.device)
+        check(lib().dgq_linear_allgather(lin.layer.handle, C.c_void_p(codes.data_ptr()), codes.stride(0),
+                                         C.c_void_p(rs.data_ptr()), M,
+                                         None if bias is None else C.c_void_p(bias.data_ptr()),
+                                         OUT_F16 if out_dtype == torch.float16 else OUT_F32,
+                                         C.c_void_p(local.data_ptr()), C.c_void_p(full.data_ptr()), self._h,
+                                         C.c_void_p(torch.cuda.current_stream(codes.device).cuda_stream)))
+        return full
+
+    def close(self):
+        from ._lib import lib
+
+        if self._h and self._h.value:
+            lib().dgq_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

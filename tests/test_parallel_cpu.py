@@ -89,3 +89,71 @@ def test_gathered_layout_roundtrip():
     full = parallel.gathered_to_full(g)
     assert full.shape == (3, 8)
     assert np.array_equal(full[:, 4:], g[1])
+
+
+class _OracleShard:
+    """A CPU stand-in for a rank's CudaLayer shard (same quantize_act / linear
+    interface), computing with the pinned C restatement: lets ColumnParallelLinear
+    itself — sharding, the gathered [p][M][N/p] layout, the all-gather and the
+    next layer's K1 on the gathered input — run over gloo without a GPU."""
+
+    def __init__(self, L, c0, c1):
+        self.P = oracle.port()
+        self.S = _to_oracle(parallel.shard_layer(L, c0 // (c1 - c0), L.o // (c1 - c0)))
+        self.w = self.P.dequantize_to_s8(self.S)
+
+    def quantize_act(self, x, codes=None, rs=None):
+        if x.dim() == 3:  # the gathered [p][M][N/p] activation, read in place on the GPU
+            x = parallel.gathered_to_full(x)
+        q, r = self.P.quantize_activations(x.float().numpy(), self.S.k, self.S.mode, self.S.act_scale)
+        return torch.from_numpy(q), torch.from_numpy(r)
+
+    def linear(self, codes, rs, bias=None, out=None, out_dtype=torch.float16):
+        acc, _ = self.P.int8_gemm(codes.numpy(), self.w)
+        y = self.P.epilogue(acc, rs.numpy(), self.S.s1)
+        if out_dtype == torch.float16:
+            return torch.from_numpy(oracle.fp16_round_np(y).astype(np.float16))
+        return torch.from_numpy(y)
+
+    def close(self):
+        pass
+
+
+def _chain_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L1 = dgq.random_layer(256, 32 * world, 64, seed=11)
+        L2 = dgq.random_layer(32 * world, 16 * world, 32, seed=12)
+        X = oracle.port().gen_synthetic(10, 256, 5, 3, 50.0, 7)
+        a = parallel.ColumnParallelLinear(L1, rank, world, shard_factory=_OracleShard)
+        b = parallel.ColumnParallelLinear(L2, rank, world, shard_factory=_OracleShard)
+        h1 = a(torch.from_numpy(X))           # [p][M][N1/p] FP16, all-gathered
+        y = b(h1, gather=True, out_dtype=torch.float32)   # K1 on the gathered layout, then gather again
+        if rank == 0:
+            P = oracle.port()
+            r1, *_ = P.dgq_forward(X, _to_oracle(L1))
+            x2 = oracle.fp16_round_np(r1).astype(np.float16).astype(np.float32)
+            r2, *_ = P.dgq_forward(x2, _to_oracle(L2))
+            full = parallel.gathered_to_full(y.numpy())
+            q.put(bool(np.array_equal(full.view(np.uint32), r2.view(np.uint32))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_column_parallel_linear_chain_over_gloo(world):
+    # two chained column-parallel linears through ColumnParallelLinear itself
+    # (FP16 all-gather between them, the next K1 reading the gathered layout):
+    # the reassembled output equals the unsharded computation bit for bit
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) is True

@@ -748,3 +748,22 @@ def test_prefill_pair_kernel_stress_10k_launches(cuda, port):
     finally:
         lib.dgq_debug_set_decode(1)
     assert launches >= 10_000
+
+
+def test_linear_allgather_c_abi_world1(cuda, port):
+    # dgq_linear_allgather over a one-rank NCCL communicator made by the C ABI
+    # (dgq_comm_unique_id / dgq_comm_create; NCCL resolved at run time): the
+    # gathered [1][M][N] output equals the plain linear bit for bit
+    from paper_2310_04836_b200 import parallel
+
+    L = oracle.random_layer(1024, 384, 128, seed=31)
+    X = port.gen_synthetic(40, 1024, 9, 3, 50.0, 3)
+    out, *_ = port.dgq_forward(X, L)
+    lin = parallel.ColumnParallelLinear(_to_dgq(L), 0, 1, device=0)
+    comm = parallel.DgqComm(0, 1, device=0)
+    codes, rs = lin.quantize(torch.from_numpy(X).cuda())
+    y = comm.linear_allgather(lin, codes, rs, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert y.shape == (1, 40, 384)
+    assert np.array_equal(bits(y[0].cpu().numpy()), bits(out))
+    comm.close()
