@@ -911,7 +911,7 @@ def run_ours(args):
                            "i8_2x_bf16_TOPS": i8_proxy}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         try:
             cpu = cpu_baseline_sample()
         except Exception as e:  # oracle not built on this box

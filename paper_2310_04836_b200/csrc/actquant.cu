@@ -180,6 +180,9 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
   const int C8 = K >> 3;
   const int cbase = part * T * V + threadIdx.x;
   const uint32_t sm = special_masks<T, V>(ksm, cbase, C8);
+  // launched with programmatic stream serialisation: everything above read
+  // layer constants only; X, Q and rs belong to the neighbouring kernels
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint4 raw[V][kF16 ? 1 : 2];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -285,6 +288,9 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
                       static_cast<uint32_t>(seg) * kEsz, &full[b]);
     }
   };
+  // launched with programmatic stream serialisation: X, Q and rs belong to the
+  // neighbouring kernels, so every thread waits for them before its first access
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int b = 0; b < depth; ++b) dgqk::mbar_init(&full[b], 1);
     dgqk::fence_mbar_init();
@@ -454,6 +460,24 @@ __global__ void k_div_check(const float* __restrict__ x, const float* __restrict
 using namespace dgqk;
 
 namespace {
+// a launch with programmatic stream serialisation (the kernel griddepcontrol.waits
+// before touching X / Q / rs, so its launch and prologue overlap the previous kernel)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 template <int T, int V, int CL, bool F16>
 cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, const float* k, const float* rk,
                        const uint8_t* ksm, int K, int Kpad, int dynamic, float act_scale, int8_t* Q, size_t ldq,
@@ -462,13 +486,15 @@ cudaError_t launch_aq2(const void* X, size_t ldx, int seg, size_t seg_stride, co
   cfg.gridDim = dim3(static_cast<unsigned>(M) * CL);
   cfg.blockDim = dim3(T);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = CL;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = CL > 1 ? 1 : 0;
+  cfg.numAttrs = CL > 1 ? 2 : 1;
   if (dynamic)
     return cudaLaunchKernelEx(&cfg, k_actquant2<T, V, CL, F16, true>, X, ldx, seg, seg_stride, k, rk, ksm, K, Kpad,
                               act_scale, Q, ldq, rs, M);
@@ -549,9 +575,8 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     int occ = 1;                                                                                                \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, smem);                                        \
     const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \
-    kern<<<grid, T_, smem, st>>>(X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K, Kpad, act_scale, Q, ldq, rs, \
-                                 M, depth);                                                                     \
-    return cudaGetLastError();                                                                                  \
+    return launch_pdl(kern, grid, T_, smem, st, X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K, Kpad,      \
+                      act_scale, Q, ldq, rs, M, depth);                                                         \
   }
 #define DGQ_AQ3_S(T_, V_, F_, D_)                                                                               \
   {                                                                                                             \
