@@ -340,8 +340,20 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
           // conversion it avoided (tools/epi_probe.cu)
 #pragma unroll
           for (int k = 0; k < 8; ++k) y[k] = __int2float_rn(static_cast<int32_t>(cur[c8 + k]));
+          // (acc * rs) * s1, two values per packed FP32x2 multiply (each RN, no contraction:
+          // the intermediate product is rounded before the second multiply, as in epilogue_f32)
+          {
+            const unsigned long long r2 = f32x2(rsm, rsm);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) y[k] = __fmul_rn(__fmul_rn(y[k], rsm), sv[k]);
+            for (int k = 0; k < 8; k += 2) {
+              unsigned long long t, u;
+              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(f32x2(y[k], y[k + 1])), "l"(r2));
+              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(u) : "l"(t), "l"(f32x2(sv[k], sv[k + 1])));
+              const float2 v = f32x2_split(u);
+              y[k] = v.x;
+              y[k + 1] = v.y;
+            }
+          }
           if (kF16Mode) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) y[k] = epilogue_f16mode(static_cast<int32_t>(cur[c8 + k]), rsm, sv[k]);
