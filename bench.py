@@ -870,13 +870,21 @@ def run_ours(args):
     k1_t = sum(a.elapsed_time(b) * 1e-3 for a, b, _, _ in layer.q_events)
     k1_b = sum(bb for _, _, bb, _ in layer.q_events)
     n_launches = len(layer.k_events) + len(layer.q_events)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    # DRAM traffic of the K5 launches from the committed ncu captures (one
+    # `ncu --set full` launch per shape, tools/profile_r02.sh): average bytes per
+    # launch over the step's six linears (q/k/v/out share the q capture)
+    traffic, traffic_by = None, None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
+    if os.path.exists(prof) and world == 1:
         try:
-            traffic = json.load(open(prof)).get("k5_fc1_dram_bytes_per_launch")
+            pr = json.load(open(prof))
+
+            def _db(k):
+                return (float(pr[k]["dram__bytes_read.sum"]) + float(pr[k]["dram__bytes_write.sum"])) * 1e6
+            traffic_by = {"q/k/v/out": _db("k5p_q"), "fc1": _db("k5p_fc1"), "fc2": _db("k5p_fc2")}
+            traffic = (4 * traffic_by["q/k/v/out"] + traffic_by["fc1"] + traffic_by["fc2"]) / 6
         except Exception:
-            traffic = None
+            traffic, traffic_by = None, None
 
     # ---- self-check of the timed outputs (after the timed region) ---------------------------
     try:
@@ -924,6 +932,11 @@ def run_ours(args):
                 except Exception as e:  # noqa: BLE001
                     detail[f"decode_m{M}_k5_streaming"] = {"error": f"{type(e).__name__}: {e}"}
         detail["k5_tops_by_linear"] = {n: o / t / 1e12 for n, (t, o) in by_name.items()}
+        if traffic_by:
+            alg = {n: k5_bytes(SEQ, K, N // world) for n, K, N in (("q/k/v/out", 7168, 7168), ("fc1", 7168, 28672),
+                                                                     ("fc2", 28672, 7168))}
+            detail["k5_dram_bytes_by_linear"] = {n: {"ncu_dram_bytes": traffic_by[n], "algorithmic_bytes": alg[n],
+                                                     "ratio": round(traffic_by[n] / alg[n], 2)} for n in alg}
         detail["k1_GBps"] = k1_b / k1_t / 1e9
         detail["k1_GBps_by_input"] = {n: x / t / 1e9 for n, (t, x) in k1_by.items()}
         plans = {n: layer.lin[n].layer.plan(SEQ) for n in ("q", "fc1", "fc2")}
