@@ -385,6 +385,7 @@ static dgq_status create_layer(int device, size_t h, size_t o, size_t g, int mod
                                const RowFetch& fetch, const uint8_t* codes_full, const int8_t* s2, const uint8_t* zp,
                                const float* s1, const float* k, size_t col_begin, size_t col_end, int validate,
                                void* stream, dgq_layer** out, cudaEvent_t* copy_done = nullptr) {
+  DGQ_NVTX("dgq_layer_create");
   if (!out) return fail(DGQ_EINVAL, "out is null");
   *out = nullptr;
   auto bad = [](const std::string& field, const std::string& m) {
@@ -779,6 +780,7 @@ dgq_status dgq_linear_plan(const dgq_layer* L, size_t M, int* token_tile, int* w
 
 dgq_status dgq_quantize_act_raw(const float* dX, size_t M, size_t K, size_t ldx, const float* dK, int mode,
                                 float act_scale, int8_t* dXq, size_t ldq, float* dRowScale, void* stream) {
+  DGQ_NVTX("dgq_quantize_act_raw");
   if (M == 0) return DGQ_OK;
   if (!dX || !dK || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
   if (ldx < K || ldq < K) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
@@ -803,6 +805,7 @@ dgq_status dgq_debug_div_check(const float* dx, const float* dk, float* dfast, f
 
 dgq_status dgq_quantize_act_f16(const dgq_layer* L, const void* dX, size_t M, size_t ldx, size_t seg_cols,
                                 size_t seg_stride, int8_t* dXq, size_t ldq, float* dRowScale, void* stream) {
+  DGQ_NVTX("dgq_quantize_act_f16");
   if (!L) return fail(DGQ_EINVAL, "null layer");
   if (M == 0) return DGQ_OK;
   if (!dX || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
@@ -818,6 +821,7 @@ dgq_status dgq_quantize_act_f16(const dgq_layer* L, const void* dX, size_t M, si
 
 dgq_status dgq_quantize_act(const dgq_layer* L, const float* dX, size_t M, size_t ldx, int8_t* dXq, size_t ldq,
                             float* dRowScale, void* stream) {
+  DGQ_NVTX("dgq_quantize_act");
   if (!L) return fail(DGQ_EINVAL, "null layer");
   if (M == 0) return DGQ_OK;
   if (!dX || !dXq || !dRowScale) return fail(DGQ_EINVAL, "null argument");
@@ -969,6 +973,7 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
 dgq_status dgq_linear(const dgq_layer* Lc, const int8_t* dXq, size_t ldq, const float* dRs, size_t M,
                       const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
                       size_t ld_acc, void* dWorkspace, size_t ws_bytes, void* stream) {
+  DGQ_NVTX("dgq_linear");
   auto* L = const_cast<dgq_layer*>(Lc);
   if (!L) return fail(DGQ_EINVAL, "null layer");
   if (M == 0) return DGQ_OK;
@@ -995,6 +1000,7 @@ dgq_status dgq_linear(const dgq_layer* Lc, const int8_t* dXq, size_t ldq, const 
 dgq_status dgq_forward_device(const dgq_layer* L, const float* dX, size_t M, size_t ldx, const float* dBias,
                               int out_dtype, void* dY, size_t ldy, int8_t* dXq, float* dRs, void* dWorkspace,
                               size_t ws_bytes, void* stream) {
+  DGQ_NVTX("dgq_forward_device");
   if (!L) return fail(DGQ_EINVAL, "null layer");
   dgq_status s = dgq_quantize_act(L, dX, M, ldx, dXq, L->k_pad, dRs, stream);
   if (s != DGQ_OK) return s;
@@ -1004,6 +1010,7 @@ dgq_status dgq_forward_device(const dgq_layer* L, const float* dX, size_t M, siz
 
 dgq_status dgq_calibrate(const float* dX, size_t rows, size_t h, size_t ldx, float percentile, int fp16_scales,
                          float* k_out, float* threshold_out, float* act_scale_out, void* stream) {
+  DGQ_NVTX("dgq_calibrate");
   if (!dX || !k_out) return fail(DGQ_EINVAL, "null argument");
   if (rows == 0 || h == 0) return fail(DGQ_EINVAL, "empty calibration set");
   if (ldx < h) return fail(DGQ_EINVAL, "leading dimension smaller than the row length");
@@ -1054,6 +1061,7 @@ dgq_status dgq_calibrate(const float* dX, size_t rows, size_t h, size_t ldx, flo
 }
 
 dgq_status dgq_layer_dequant_s8(const dgq_layer* L, int8_t* dW, size_t ldw, void* stream) {
+  DGQ_NVTX("dgq_layer_dequant_s8");
   if (!L || !dW) return fail(DGQ_EINVAL, "null argument");
   if (ldw < L->o) return fail(DGQ_EINVAL, "ldw smaller than the shard width");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1111,6 +1119,7 @@ dgq_status dgq_audit_max_abs_acc(const int8_t* dXq, size_t ldx, const int8_t* dW
 
 dgq_status dgq_int8_gemm(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t ldw, size_t M, size_t K, size_t N,
                          int32_t* dAcc, size_t ld_acc, int64_t* max_abs_acc, void* stream) {
+  DGQ_NVTX("dgq_int8_gemm");
   if (static_cast<double>(K) * 127.0 * 127.0 >= 2147483648.0)
     return fail(DGQ_EINVAL, "h too large for 32-bit accumulation");
   if (max_abs_acc) *max_abs_acc = 0;
@@ -1170,6 +1179,7 @@ dgq_status dgq_epilogue(const int32_t* dAcc, size_t lda, const float* dRs, const
 dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int8_t* dXq, size_t ldq,
                             const float* dRowScale, size_t M, const float* const* dBias, int out_dtype,
                             void* const* dY, const size_t* ldy, void* dWorkspace, size_t ws_bytes, void* stream) {
+  DGQ_NVTX("dgq_linear_multi");
   if (!layers || count < 1 || count > kDecodeMaxSub || !dY || !ldy)
     return fail(DGQ_EINVAL, "dgq_linear_multi: 1..4 layers with outputs");
   const dgq_layer* L0 = layers[0];
@@ -1238,6 +1248,7 @@ static dgq_status upload_grid(const float* grid, size_t n, float** d, cudaStream
 dgq_status dgq_phase1_search(const float* dW, size_t h, size_t o, const float* dX, const float* dXhat, size_t b,
                              size_t g, int n_bits, const float* alpha_grid, size_t n_alpha, float* dSprime,
                              int32_t* dZp, float* dErr, float* dAlpha, uint64_t* evals, void* stream) {
+  DGQ_NVTX("dgq_phase1_search");
   // SearchConfig::validate (proj/src/search.cpp:24-45)
   if (g < 1 || h % g != 0)
     return fail(DGQ_EINVAL, "group size " + std::to_string(g) + " must divide h = " + std::to_string(h));
@@ -1277,6 +1288,7 @@ dgq_status dgq_phase2_search(const float* dW, size_t h, size_t o, const float* d
                              size_t g, const float* dSprime, const int32_t* dZp, const float* alpha_grid,
                              size_t n_alpha, float* dS1, int8_t* dS2, int32_t* dCodes, double* dColErr,
                              float* dColAlpha, uint64_t* evals, void* stream) {
+  DGQ_NVTX("dgq_phase2_search");
   if (g == 0 || h % g != 0) return fail(DGQ_EINVAL, "GroupParams shape does not match weights");
   if (!alpha_grid || n_alpha == 0) return fail(DGQ_EINVAL, "alpha_grid_phase2 is empty");
   if (evals) *evals = static_cast<uint64_t>(o) * n_alpha;

@@ -337,6 +337,7 @@ dgq_status dgq_host_forward(size_t M, size_t h, size_t o, size_t g, int mode, fl
 
 dgq_status dgq_layer_forward_host(const dgq_layer* layer, const float* X, size_t M, const float* dBias,
                                   int out_dtype, void* Y, void* stream) {
+  DGQ_NVTX("dgq_layer_forward_host");
   if (!layer) return dgq_internal_fail(DGQ_EINVAL, "null layer", "");
   if (M == 0) return DGQ_OK;
   if (!X || !Y) return dgq_internal_fail(DGQ_EINVAL, "null argument", "");

@@ -166,6 +166,15 @@ cudaError_t dgq_launch_phase2(const float* W, const float* X, const float* Xhat,
 // issuing `blocks` x 4 tcgen05.mma.cta_group::2.kind::i8 of 256 x 256 x 32.
 cudaError_t dgq_launch_i8_peak(int pairs, int blocks, unsigned long long* sink, cudaStream_t st);
 
+// NVTX range around a C-ABI entry point (visible in Nsight Systems / ncu
+// --nvtx; a few tens of ns per call when no tool is attached).
+#include <nvtx3/nvToolsExt.h>
+struct DgqNvtxRange {
+  explicit DgqNvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~DgqNvtxRange() { nvtxRangePop(); }
+};
+#define DGQ_NVTX(name) DgqNvtxRange dgq_nvtx_range_(name)
+
 // Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum,
 // once per (kernel, device) under a lock, so concurrent launches of one
 // instantiation with different sizes never shrink each other's limit.
