@@ -118,6 +118,9 @@ __device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t parity)
       : "memory");
   return ok != 0;
 }
+#ifndef DGQ_PF_LATE_TRIGGER
+#define DGQ_PF_LATE_TRIGGER 0  // tools: 1 triggers dependents at the end of the epilogue (A/B)
+#endif
 #ifndef DGQ_PF_RELAXED_READY
 #define DGQ_PF_RELAXED_READY 0  // tools: 1 drops the release fence before the ready arrive (A/B of its cost)
 #endif
@@ -544,6 +547,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
   float* s_bias = s_s1 + 256;                              // [TN]
 
   const uint32_t warp = warp_id(), lane = lane_id();
+#if !DGQ_PF_LATE_TRIGGER
+  // Dependents may be scheduled as soon as SMs free up: the next kernel's CTAs
+  // fill the SMs this launch's early-finishing pairs leave (stream-K tail)
+  // and start streaming their weights; they griddepcontrol.wait before
+  // touching anything this kernel writes.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSA; ++s) {
       mbar_init(&afull[s], 1);
@@ -971,7 +981,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
       p.dbg[8 * 1024 + blockIdx.x] = g;
     }
+#if DGQ_PF_LATE_TRIGGER
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   }
   tc_fence_before();
   cooperative_groups::this_cluster().sync();
