@@ -327,6 +327,15 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
     uint32_t r[2][16];
     tmem_ld16(tbase + c0, r[0]);
     tmem_ld_wait();
+    if (p.dbg_flags & 4) {  // tools (mode bit 20): TMEM loads only
+      for (int c16 = 16; c16 < kCB; c16 += 16) {
+        tmem_ld16(tbase + c0 + c16, r[1]);
+        tmem_ld_wait();
+        r[0][0] ^= r[1][0];
+      }
+      if (r[0][0] == 0x7FFFFFFFu) myrow[0] = 1;
+      continue;
+    }
 #pragma unroll
     for (int c16 = 0; c16 < kCB; c16 += 16) {
       uint32_t (&cur)[16] = r[(c16 / 16) & 1];
@@ -394,6 +403,7 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
       if (c16 + 16 < kCB) tmem_ld_wait();
     }
     __syncwarp();
+    if (p.dbg_flags & 2) continue;  // tools (mode bit 19): no global stores
     // 8 passes x (4 rows x 8 lanes x 16 bytes)
     const int ch = static_cast<int>(lane & 7);                 // 16-byte chunk of the row segment
     const int n = nbase + c0 + ch * (kF16 ? 8 : 4);            // first output column of the chunk
