@@ -142,8 +142,10 @@ dgq_status dgq_linear(const dgq_layer* layer, const int8_t* dXq, size_t ldq, con
 /* Several layers that share the input (q / k / v of a decoder layer, gate / up
  * of an MLP): `count` (1..4) outputs from one activation-code buffer.  Decode-
  * shaped calls (M <= 32) run as ONE K5d launch over the concatenation of the
- * layers' weight tiles (one stream-K problem: fewer launches, better balance);
- * other shapes fall back to one dgq_linear per layer.  Layers must share h, g.
+ * layers' weight tiles, prefill-shaped calls (the pair kernel's M range) as ONE
+ * K5p launch over their pair tiles (one stream-K problem: fewer launches, one
+ * tail, better balance); other shapes fall back to one dgq_linear per layer.
+ * Layers must share h, g.
  * dBias may be NULL or hold NULL entries; dY[i] is [M x ldy[i]].  dWorkspace:
  * dgq_linear_multi_workspace_bytes zeroed bytes, or NULL for layers[0]'s own. */
 dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int8_t* dXq, size_t ldq,

@@ -314,8 +314,9 @@ class CudaLayer:
 # ---------------------------------------------------------------------------
 
 def linear_multi(layers, codes: torch.Tensor, rs: torch.Tensor, outs=None, biases=None, out_dtype=torch.float16):
-    """Several CudaLayers that share the input (q/k/v): one K5d launch over all of
-    their weight tiles for decode-shaped M (dgq_linear_multi); returns the outputs."""
+    """Several CudaLayers that share the input (q/k/v): one launch over all of
+    their weight tiles — K5d for decode-shaped M, K5p for prefill-shaped M
+    (dgq_linear_multi); returns the outputs."""
     n = len(layers)
     M = codes.shape[0]
     if outs is None:

@@ -896,11 +896,23 @@ static dgq_status run_decode(const DecodeSub* subs, int count, int g, size_t k_p
   return DGQ_OK;
 }
 
-static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& tmA, int g, size_t N, size_t k_pad,
-                           const int8_t* dXq, size_t ldq, size_t M, const float* dRs, const float* dS1,
-                           const float* dBias, int out_dtype, int fp16_mode, void* dY, size_t ldy, int32_t* dAcc,
-                           size_t ld_acc, void* ws, size_t ws_bytes, cudaStream_t st) {
+// One fused linear launch.  `count` > 1: layers sharing the input run as one
+// K5p stream-K problem over the concatenation of their pair tiles (prefill-
+// shaped calls of dgq_linear_multi; the caller checked the plan is K5p).
+static dgq_status run_gemm(bool fused, const DecodeSub* subs, int count, const CUtensorMap& tmA, int g, size_t k_pad,
+                           const int8_t* dXq, size_t ldq, size_t M, const float* dRs, int out_dtype, int fp16_mode,
+                           int32_t* dAcc, size_t ld_acc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const uint8_t* tiles = subs[0].tiles;
+  const float *dS1 = subs[0].s1, *dBias = subs[0].bias;
+  void* dY = subs[0].out;
+  const size_t ldy = subs[0].ldy;
+  size_t N = static_cast<size_t>(subs[0].N);
+  if (count > 1) {  // plan on the concatenation (128-channel tiles)
+    N = 0;
+    for (int i = 0; i < count; ++i) N += static_cast<size_t>((subs[i].N + 127) / 128) * 128;
+  }
   DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), static_cast<int>(N), static_cast<int>(k_pad), fused, g);
+  if (count > 1 && !pl.prefill2) return fail(DGQ_EINVAL, "multi-layer launch is only planned for the pair kernel");
   if (pl.ws_bytes + pl.counter_bytes > ws_bytes)
     return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(pl.ws_bytes + pl.counter_bytes));
   CUtensorMap tmB{};
@@ -940,12 +952,14 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
   {
     const size_t esz = out_dtype == DGQ_OUT_F16 ? 2 : 4;
     bool ok = true;
-    if (dY) ok = ok && (reinterpret_cast<uintptr_t>(dY) % 16 == 0) && ((ldy * esz) % 16 == 0);
+    for (int i = 0; i < count; ++i)
+      if (subs[i].out)
+        ok = ok && (reinterpret_cast<uintptr_t>(subs[i].out) % 16 == 0) && ((subs[i].ldy * esz) % 16 == 0);
     if (dAcc) ok = ok && (reinterpret_cast<uintptr_t>(dAcc) % 16 == 0) && ((ld_acc * 4) % 16 == 0);
     p.vec_ok = ok ? 1 : 0;
   }
   CUtensorMap tmY{};
-  if (pl.bn >= 128 && dY && p.vec_ok) {
+  if (pl.bn >= 128 && dY && p.vec_ok && count == 1) {
     dgq_status ys = make_out_tmap(&tmY, dY, M, N, ldy, out_dtype == DGQ_OUT_F16);
     if (ys != DGQ_OK) return ys;
     p.tma_out = 1;
@@ -957,6 +971,13 @@ static dgq_status run_gemm(bool fused, const uint8_t* tiles, const CUtensorMap& 
     if (ms != DGQ_OK) return ms;
     p.chunk_stride = p.chunk_bytes;
     p.dbg_flags = (dgq_debug_decode_mode() >> 18) & 31;  // tools: mode bits 18-22
+    p.nsub = count;
+    int tb = 0;
+    for (int i = 0; i < count; ++i) {
+      p.sub[i] = DgqDecodeSub{subs[i].tiles, subs[i].s1, subs[i].bias, subs[i].out, subs[i].ldy, subs[i].N, tb};
+      tb += (subs[i].N + pl.pair_tn - 1) / pl.pair_tn;
+    }
+    p.n_pair_tiles = tb;
     if (pl.stream_k) {
       if (!ws) return fail(DGQ_EINVAL, "stream-K prefill kernel needs a workspace");
       p.stream_k = 1;
@@ -982,19 +1003,20 @@ dgq_status dgq_linear(const dgq_layer* Lc, const int8_t* dXq, size_t ldq, const 
     if (s != DGQ_OK) return s;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const DecodeSub one{L->tiles, L->s1, dBias, dY, ldy, static_cast<int>(L->o)};
   const size_t need = dgq_linear_workspace_bytes(L, M);
   void* ws = dWorkspace;
   if (need && !ws) {
     std::lock_guard<std::mutex> lk(L->ws_mu);
     dgq_status s = ws_acquire(L, st, need, &ws, &ws_bytes);
     if (s != DGQ_OK) return s;
-    s = run_gemm(L->fused, L->tiles, L->tmA, static_cast<int>(L->g), L->o, L->k_pad, dXq, ldq, M, dRs, L->s1, dBias,
-                 out_dtype, fp16_mode, dY, ldy, dAcc, ld_acc, ws, ws_bytes, st);
+    s = run_gemm(L->fused, &one, 1, L->tmA, static_cast<int>(L->g), L->k_pad, dXq, ldq, M, dRs, out_dtype, fp16_mode,
+                 dAcc, ld_acc, ws, ws_bytes, st);
     ws_release(L, st);
     return s;
   }
-  return run_gemm(L->fused, L->tiles, L->tmA, static_cast<int>(L->g), L->o, L->k_pad, dXq, ldq, M, dRs, L->s1,
-                  dBias, out_dtype, fp16_mode, dY, ldy, dAcc, ld_acc, ws, ws_bytes, st);
+  return run_gemm(L->fused, &one, 1, L->tmA, static_cast<int>(L->g), L->k_pad, dXq, ldq, M, dRs, out_dtype, fp16_mode,
+                  dAcc, ld_acc, ws, ws_bytes, st);
 }
 
 dgq_status dgq_forward_device(const dgq_layer* L, const float* dX, size_t M, size_t ldx, const float* dBias,
@@ -1153,9 +1175,10 @@ dgq_status dgq_int8_gemm(const int8_t* dXq, size_t ldx, const int8_t* dW, size_t
     DGQ_CUDA(cudaMallocAsync(&ws, need, st));
     DGQ_CUDA(cudaMemsetAsync(ws, 0, need, st));
   }
-  if (s == DGQ_OK)
-    s = run_gemm(false, nullptr, tmA, 128, N, k_pad, xq, k_pad, M, nullptr, nullptr, nullptr, DGQ_OUT_F32, 0, nullptr,
-                 0, dAcc, ld_acc, ws, need, st);
+  if (s == DGQ_OK) {
+    const DecodeSub plain{nullptr, nullptr, nullptr, nullptr, 0, static_cast<int>(N)};
+    s = run_gemm(false, &plain, 1, tmA, 128, k_pad, xq, k_pad, M, nullptr, DGQ_OUT_F32, 0, dAcc, ld_acc, ws, need, st);
+  }
   if (s == DGQ_OK && max_abs_acc) s = dgq_audit_max_abs_acc(dXq, ldx, dW, ldw, M, K, N, max_abs_acc, stream);
   if (ws) cudaFreeAsync(ws, st);
   if (wdense) cudaFreeAsync(wdense, st);
@@ -1199,7 +1222,31 @@ dgq_status dgq_linear_multi(const dgq_layer* const* layers, int count, const int
   for (int i = 0; i < count; ++i) total_tiles += layers[i]->n_tiles;
   DgqGemmPlan pl = dgq_plan_gemm(static_cast<int>(M), total_tiles * 128, static_cast<int>(L0->k_pad), L0->fused,
                                  static_cast<int>(L0->g));
-  if (!pl.decode) {  // not decode-shaped: one launch per layer
+  if (pl.prefill2 && L0->fused) {
+    // prefill-shaped: one K5p stream-K problem over the layers' pair tiles
+    // (one launch, one tail, instead of one per layer)
+    DecodeSub subs[kDecodeMaxSub];
+    for (int i = 0; i < count; ++i)
+      subs[i] = DecodeSub{layers[i]->tiles, layers[i]->s1, dBias ? dBias[i] : nullptr, dY[i], ldy[i],
+                          static_cast<int>(layers[i]->o)};
+    const size_t need = pl.ws_bytes + pl.counter_bytes;
+    if (dWorkspace) {
+      if (ws_bytes < need) return fail(DGQ_EINVAL, "workspace too small: need " + std::to_string(need));
+      return run_gemm(true, subs, count, L0->tmA, static_cast<int>(L0->g), L0->k_pad, dXq, ldq, M, dRowScale,
+                      out_dtype, 0, nullptr, 0, dWorkspace, ws_bytes, st);
+    }
+    auto* L = const_cast<dgq_layer*>(L0);
+    std::lock_guard<std::mutex> lk(L->ws_mu);
+    void* ws = nullptr;
+    size_t cap = 0;
+    dgq_status s = ws_acquire(L, st, need, &ws, &cap);
+    if (s != DGQ_OK) return s;
+    s = run_gemm(true, subs, count, L0->tmA, static_cast<int>(L0->g), L0->k_pad, dXq, ldq, M, dRowScale, out_dtype, 0,
+                 nullptr, 0, ws, cap, st);
+    ws_release(L, st);
+    return s;
+  }
+  if (!pl.decode) {  // neither decode- nor pair-kernel-shaped: one launch per layer
     for (int i = 0; i < count; ++i) {
       dgq_status s = dgq_linear(layers[i], dXq, ldq, dRowScale, M, dBias ? dBias[i] : nullptr, out_dtype, 0, dY[i],
                                 ldy[i], nullptr, 0, nullptr, 0, stream);

@@ -33,6 +33,21 @@ inline bool fused_ok(int g) {
 }
 }  // namespace dgq_layout
 
+// Layers that share one input (e.g. q / k / v) and run as ONE stream-K
+// problem over the concatenation of their weight tiles: K5d (decode.cu, up to
+// kDecodeMaxSub layers) and K5p (prefill.cu).  tile_begin = the layer's first
+// tile of the concatenation (K5d: 128-channel tiles; K5p: pair tiles).
+constexpr int kDecodeMaxSub = 4;
+struct DgqDecodeSub {
+  const uint8_t* tiles;
+  const float* s1;
+  const float* bias;
+  void* out;
+  size_t ldy;
+  int N;
+  int tile_begin;  // first global tile of this layer
+};
+
 struct DgqGemmParams {
   // A side (weights): prepared INT4 tiles (fused) or via tensor map (plain int8)
   const uint8_t* tiles;
@@ -59,22 +74,13 @@ struct DgqGemmParams {
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (debug builds of tools/)
   int stream_k;             // K5p: stream-K over (tile, k-block) units (ws / counters = pair slots / flags)
   int dbg_flags;            // tools only (K5p): 16 = 256-token tiles keep the TMA-store epilogue
+  // K5p: the layers of the launch (nsub >= 1; a single layer is sub[0]) and
+  // the total number of TN-wide pair tiles over all of them
+  int nsub;
+  int n_pair_tiles;
+  DgqDecodeSub sub[kDecodeMaxSub];
 };
 
-// K5d (decode.cu): stream-K over (weight tile, k-block) units, (code - ZP) as
-// the signed A operand from TMEM, group scales applied to TMEM partials.
-// Up to kDecodeMaxSub layers that share the input (e.g. q / k / v) form ONE
-// stream-K problem over the concatenation of their weight tiles.
-constexpr int kDecodeMaxSub = 4;
-struct DgqDecodeSub {
-  const uint8_t* tiles;
-  const float* s1;
-  const float* bias;
-  void* out;
-  size_t ldy;
-  int N;
-  int tile_begin;  // first global tile of this layer
-};
 struct DgqDecodeParams {
   int nsub;  // number of layers (1 = the single-layer fields below are mirrored in sub[0])
   DgqDecodeSub sub[kDecodeMaxSub];

@@ -308,20 +308,20 @@ __device__ __forceinline__ size_t part_off(int c16, int v, int row) {
 // per instruction; tools/pf_trace.py measured an 11 us epilogue that way, and
 // a TMA store per 64 columns serialises on its issue latency).
 template <int TN, bool kF16, bool kFlush>
-__device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbase, float rsm, const float* s_s1,
-                                           const float* s_bias, uint8_t* stg, int mrow0, int nbase, int cbeg,
-                                           int cend) {
+__device__ __forceinline__ void epi_direct(const DgqGemmParams& p, const DgqDecodeSub& d, uint32_t tbase, float rsm,
+                                           const float* s_s1, const float* s_bias, uint8_t* stg, int mrow0, int nbase,
+                                           int cbeg, int cend) {
   // the FP16 epilogue mode and the bias are uniform runtime branches: every
   // template variant unrolled here cost instruction-cache misses (the kernel's
   // SASS reached 350 KB and the exposed epilogue ran at ~1/6 of its issue rate)
-  const bool kF16Mode = p.fp16_mode != 0, kBias = p.bias != nullptr;
+  const bool kF16Mode = p.fp16_mode != 0, kBias = d.bias != nullptr;
   constexpr int kCB = kF16 ? 64 : 32;  // columns per 128-byte row segment
   const uint32_t lane = lane_id();
   uint8_t* myrow = stg + lane * 128;
   const uint32_t sw = lane & 7;
 #pragma unroll 1
   for (int c0 = cbeg; c0 < cend; c0 += kCB) {
-    if (nbase + c0 >= p.N) break;
+    if (nbase + c0 >= d.N) break;
     // 16-column TMEM loads, the next one in flight while this one is converted
     // (a whole 64-column batch in registers spilled: 96 registers per thread)
     uint32_t r[2][16];
@@ -408,9 +408,9 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
     const int ch = static_cast<int>(lane & 7);                 // 16-byte chunk of the row segment
     const int n = nbase + c0 + ch * (kF16 ? 8 : 4);            // first output column of the chunk
     constexpr int kPer = kF16 ? 8 : 4;                         // outputs per chunk
-    uint8_t* const out0 = static_cast<uint8_t*>(p.out) + (static_cast<size_t>(mrow0) * p.ldy + n) * (kF16 ? 2 : 4);
-    const size_t row_bytes = p.ldy * (kF16 ? 2 : 4);
-    if (mrow0 + 32 <= p.M && nbase + c0 + kCB <= p.N) {
+    uint8_t* const out0 = static_cast<uint8_t*>(d.out) + (static_cast<size_t>(mrow0) * d.ldy + n) * (kF16 ? 2 : 4);
+    const size_t row_bytes = d.ldy * (kF16 ? 2 : 4);
+    if (mrow0 + 32 <= p.M && nbase + c0 + kCB <= d.N) {
       // interior block: no per-store bounds checks (branches cost the exposed epilogue)
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
@@ -426,11 +426,11 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
         const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
         if (m < p.M) {
           uint8_t* dst = out0 + row * row_bytes;
-          if (n + kPer <= p.N) {
+          if (n + kPer <= d.N) {
             *reinterpret_cast<uint4*>(dst) = v;
-          } else if (n < p.N) {
+          } else if (n < d.N) {
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-            for (int k = 0; k < kPer && n + k < p.N; ++k) {
+            for (int k = 0; k < kPer && n + k < d.N; ++k) {
               if (kF16)
                 reinterpret_cast<uint16_t*>(dst)[k] = static_cast<uint16_t>(w[k >> 1] >> ((k & 1) * 16));
               else
@@ -447,7 +447,7 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, uint32_t tbas
 // 32 token rows (this warp's TMEM lane quadrant) x 256 channels of one
 // accumulator -> scales -> FP16/FP32 -> swizzled staging -> TMA store.
 template <int TN, bool kF16, bool kF16Mode, bool kBias>
-__device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase, float rsm, const float* s_s1,
+__device__ __forceinline__ void epi_rows(const DgqGemmParams& p, int N, uint32_t tbase, float rsm, const float* s_s1,
                                          const float* s_bias, uint8_t* stg0, const CUtensorMap* tmY, int nbase,
                                          int mbox) {
   constexpr int kCB = kF16 ? 64 : 32;  // columns per 128-byte box row
@@ -456,7 +456,7 @@ __device__ __forceinline__ void epi_rows(const DgqGemmParams& p, uint32_t tbase,
   const uint32_t sw = lane & 7;
 #pragma unroll 1
   for (int c0 = 0; c0 < TN; c0 += kCB) {
-    if (nbase + c0 >= p.N) break;
+    if (nbase + c0 >= N) break;
     uint32_t r[kCB];
 #pragma unroll
     for (int c1 = 0; c1 < kCB; c1 += 16) tmem_ld16(tbase + c0 + c1, *reinterpret_cast<uint32_t(*)[16]>(&r[c1]));
@@ -523,13 +523,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int KB = p.k_blocks;
-  const int n_tiles = (p.N + 127) / 128;  // 128-channel weight tiles (prepared chunks)
   // tiles are token-tile major (t = mt * n_pairs + nt): the stream-K ranges of
   // the pairs working on different token tiles sweep the same weight tiles at
   // the same time, so each weight chunk comes from HBM once and is re-read from
   // L2 (n-major order re-read every chunk per token tile: 3.7x the unique HBM
   // bytes on OPT-30B fc1, profiles/ncu_summary_r01c.json)
-  const int m_pairs = (p.M + 256 * S - 1) / (256 * S), n_pairs = (p.N + TN - 1) / TN;
+  const int m_pairs = (p.M + 256 * S - 1) / (256 * S), n_pairs = p.n_pair_tiles;
+  // pair tile nt (of the concatenation) -> its layer (several layers sharing
+  // the input run as one problem; a single layer is sub[0])
+  auto sub_of = [&](int nt) {
+    int i = 0;
+    while (i + 1 < p.nsub && nt >= p.sub[i + 1].tile_begin) ++i;
+    return i;
+  };
+  // this CTA's 128-channel prepared tile of pair tile nt inside its layer
+  // (TN = 128: both CTAs dequantise halves of the same one) and whether it exists
+  auto ctile_of = [&](int nt, int& sub, int& ctile) {
+    sub = sub_of(nt);
+    const int ntl = nt - p.sub[sub].tile_begin;
+    ctile = TN == 256 ? ntl * 2 + static_cast<int>(rank) : ntl;
+    return ctile < (p.sub[sub].N + 127) / 128;
+  };
   const int total = m_pairs * n_pairs;
   const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
 
@@ -615,16 +629,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
         const int t = c.t, kb = c.kb;
         si.advance(c);
         si.advance(c);
-        const int nt = t % n_pairs;
+        int sub, ctile;
         // the prepared 128-channel weight tile this CTA dequantises (from)
-        const int ctile = TN == 256 ? nt * 2 + static_cast<int>(rank) : nt;
-        const bool has_w = ctile < n_tiles;
+        const bool has_w = ctile_of(t % n_pairs, sub, ctile);
         const int s = i % kSC;
         wait_local(&cempty[s], ((i / kSC) & 1) ^ 1, 1);
         pf_stamp(p, 1, i);
         mbar_arrive_expect_tx(&cfull[s], has_w ? p.chunk_bytes : 0u);
         if (has_w)
-          bulk_load(sC + s * p.chunk_stride, p.tiles + (static_cast<size_t>(ctile) * KB + kb) * p.chunk_bytes,
+          bulk_load(sC + s * p.chunk_stride, p.sub[sub].tiles + (static_cast<size_t>(ctile) * KB + kb) * p.chunk_bytes,
                     p.chunk_bytes, &cfull[s]);
       }
     }
@@ -733,8 +746,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
       for (int it = grp; it < n; it += kDqGroups) {
         const int t = cu.t;
         for (int i = 0; i < kDqGroups; ++i) si.advance(cu);
-        const int nt = t % n_pairs;
-        const bool has_w = (TN == 256 ? nt * 2 + static_cast<int>(rank) : nt) < n_tiles;
+        int sub_, ctile_;
+        const bool has_w = ctile_of(t % n_pairs, sub_, ctile_);
         const int s = it % kSC, b = it % kSB;
         wait_local(&cfull[s], (it / kSC) & 1, 4);
         if ((warp & 3) == 0 && lane == 0) pf_stamp(p, 2, it);
@@ -809,14 +822,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
     const long long U = static_cast<long long>(total) * KB;
     constexpr size_t kSub = 128 * TN;    // ints of one 128-row partial
     constexpr size_t kSlot = S * kSub;   // ints per CTA partial (S sub-tiles)
-    const bool b_ = p.bias != nullptr, f_ = p.fp16_mode != 0;
+    const bool f_ = p.fp16_mode != 0;
     uint32_t fphase = 0;
     int t, lo, hi;
     for (; si.next(t, lo, hi); ++tl) {
       const int mt = t / n_pairs, nt = t % n_pairs;
       const int acc = tl % kNAcc;
       const uint32_t tpar = (tl / kNAcc) & 1;
-      const int n0 = nt * TN;
+      const DgqDecodeSub& d = p.sub[sub_of(nt)];  // this tile's layer
+      const int n0 = (nt - d.tile_begin) * TN;      // first channel of the tile inside its layer
+      const bool b_ = d.bias != nullptr;
       const int mrow = q * 32 + lane;
       // sub-tile `sub` of this CTA: token rows mt*256S + sub*256 + rank*128 + [0, 128)
       auto m0_of = [&](int sub) { return mt * 256 * S + sub * 256 + static_cast<int>(rank) * 128; };
@@ -862,8 +877,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
         s_rs[i] = (p.rs && mm < p.M) ? p.rs[mm] : 0.0f;
       }
       for (int i = et; i < TN; i += kEpiThreads) {
-        s_s1[i] = (p.s1 && n0 + i < p.N) ? p.s1[n0 + i] : 0.0f;
-        s_bias[i] = (p.bias && n0 + i < p.N) ? p.bias[n0 + i] : 0.0f;
+        s_s1[i] = (d.s1 && n0 + i < d.N) ? d.s1[n0 + i] : 0.0f;
+        s_bias[i] = (d.bias && n0 + i < d.N) ? d.bias[n0 + i] : 0.0f;
       }
       if (npart) {
         for (int c = 1; c <= npart; ++c) {
@@ -919,7 +934,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
         const float rsm = s_rs[sub * 128 + mrow];
         if (et == 0 && tl < 8) pf_stamp(p, 9, 512 + 4 * tl + sub);
         if (m0 >= p.M) continue;  // a token quarter past M: nothing to store
-        if (p.out && p.vec_ok && !p.acc_out && !(S == 1 && (p.dbg_flags & 16))) {  // tools: 16 = S=1 TMA epilogue
+        if (d.out && p.vec_ok && !p.acc_out && !(S == 1 && (p.dbg_flags & 16))) {  // tools: 16 = S=1 TMA epilogue
           {
             // No value of this warp's rows can land in fp16_round's flush range
             // (0 < |y| < 2^-24) when rs * min(s1) >= 2^-24: |acc| >= 1 for every
@@ -927,21 +942,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
             float s1min = 3.0e38f;
             for (int c = cbeg + static_cast<int>(lane); c < cend; c += 32) s1min = fminf(s1min, s_s1[c]);
             for (int o = 16; o > 0; o >>= 1) s1min = fminf(s1min, __shfl_xor_sync(0xffffffffu, s1min, o));
-            const bool safe = !p.bias && !p.fp16_mode && __fmul_rn(rsm, s1min) >= 0x1p-24f;
+            const bool safe = !d.bias && !p.fp16_mode && __fmul_rn(rsm, s1min) >= 0x1p-24f;
             if (p.out_f16) {
               if (__all_sync(0xffffffffu, safe))
-                epi_direct<TN, true, false>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+                epi_direct<TN, true, false>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
               else
-                epi_direct<TN, true, true>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+                epi_direct<TN, true, true>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
             } else {
-              epi_direct<TN, false, true>(p, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+              epi_direct<TN, false, true>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
             }
           }
         } else if (S == 1 && p.tma_out && !p.acc_out) {
           if constexpr (S == 1) {
             const int mbox = m0 + q * 32;
 #define DGQ_EPI2(F16_, MODE_, BIAS_) \
-  epi_rows<TN, F16_, MODE_, BIAS_>(p, tbase, rsm, s_s1, s_bias, stg0, &tmY, n0, mbox)
+  epi_rows<TN, F16_, MODE_, BIAS_>(p, d.N, tbase, rsm, s_s1, s_bias, stg0, &tmY, n0, mbox)
             if (p.out_f16) {
               if (f_) { if (b_) DGQ_EPI2(true, true, true); else DGQ_EPI2(true, true, false); }
               else    { if (b_) DGQ_EPI2(true, false, true); else DGQ_EPI2(true, false, false); }
@@ -955,7 +970,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
           const int m = m0 + mrow;
 #pragma unroll 1
           for (int c0 = cbeg; c0 < cend; c0 += 16) {
-            if (n0 + c0 >= p.N) break;
+            if (n0 + c0 >= d.N) break;
             uint32_t r[16];
             tmem_ld16(tbase + c0, r);
             tmem_ld_wait();
@@ -963,16 +978,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const int n = n0 + c0 + k;
-              if (n >= p.N) break;
+              if (n >= d.N) break;
               const int32_t a = static_cast<int32_t>(r[k]);
               if (p.acc_out) p.acc_out[static_cast<size_t>(m) * p.ld_acc + n] = a;
-              if (p.out) {
+              if (d.out) {
                 float y = p.fp16_mode ? epilogue_f16mode(a, rsm, s_s1[c0 + k]) : epilogue_f32(a, rsm, s_s1[c0 + k]);
-                if (p.bias) y = __fadd_rn(y, s_bias[c0 + k]);
+                if (d.bias) y = __fadd_rn(y, s_bias[c0 + k]);
                 if (p.out_f16)
-                  static_cast<__half*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = fp16_ref(y);
+                  static_cast<__half*>(d.out)[static_cast<size_t>(m) * d.ldy + n] = fp16_ref(y);
                 else
-                  static_cast<float*>(p.out)[static_cast<size_t>(m) * p.ldy + n] = y;
+                  static_cast<float*>(d.out)[static_cast<size_t>(m) * d.ldy + n] = y;
               }
             }
           }
@@ -1075,7 +1090,7 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
   cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.N, TN, p.k_blocks, p.stream_k != 0, S));
+  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.n_pair_tiles * TN, TN, p.k_blocks, p.stream_k != 0, S));
   cfg.blockDim = dim3(pf::Cfg<S, TN>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

@@ -427,6 +427,38 @@ def test_linear_multi_shared_input(cuda, port, decode_kernel, M):
         assert np.array_equal(bits(a.cpu().numpy()), bits(b.cpu().numpy()))
 
 
+MULTI_PREFILL_CASES = [
+    # (M, h, widths, g): q / k / v style layers over one input as ONE pair-kernel
+    # launch; ragged widths put layer boundaries inside pair tiles' neighbours
+    (256, 1024, (256, 384, 130), 128), (600, 2048, (512, 300, 768), 64), (1100, 1536, (1000, 1000, 1000), 128),
+    (512, 992, (130, 2, 258, 640), 32),
+]
+
+
+@pytest.mark.parametrize("M,h,widths,g", MULTI_PREFILL_CASES)
+def test_linear_multi_prefill_one_pair_launch(cuda, port, pair_kernel, M, h, widths, g):
+    # prefill-shaped dgq_linear_multi: the layers' pair tiles form one stream-K
+    # problem (csrc/prefill.cu sub_of / ctile_of); every layer's output must
+    # equal its own dgq_forward bit for bit, FP32 and FP16, with and without bias
+    Ls = [oracle.random_layer(h, o, g, seed=o + i) for i, o in enumerate(widths)]
+    for L in Ls[1:]:
+        L.k = Ls[0].k
+    X = port.gen_synthetic(M, h, 7 + M, 3, 50.0, 3)
+    CLs = [dgq.CudaLayer(_to_dgq(L)) for L in Ls]
+    codes, drs = CLs[0].quantize_act(torch.from_numpy(X).cuda())
+    rng = np.random.default_rng(M)
+    bnp = [None if i % 2 == 0 else rng.uniform(-1, 1, o).astype(np.float32) for i, o in enumerate(widths)]
+    biases = [None if b is None else torch.from_numpy(b).cuda() for b in bnp]
+    refs = [port.dgq_forward(X, L, b)[0] for L, b in zip(Ls, bnp)]
+    for _ in range(2):  # twice: the stream-K workspace and flags are left re-armed
+        outs = dgq.linear_multi(CLs, codes, drs, biases=biases, out_dtype=torch.float32)
+        for i, ref in enumerate(refs):
+            assert np.array_equal(bits(outs[i].cpu().numpy()), bits(ref)), i
+    outs16 = dgq.linear_multi(CLs, codes, drs, biases=biases, out_dtype=torch.float16)
+    for i, ref in enumerate(refs):
+        assert np.array_equal(bits(outs16[i].cpu().numpy()), bits(port.fp16_round_array(ref).astype(np.float16))), i
+
+
 def test_decode_and_prefill_orientations_agree(cuda, port):
     import ctypes
 
