@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -842,6 +843,19 @@ struct DecodeSub {
   int N;
 };
 
+// K5d stages whose weight chunks are requested before the kernel waits for its
+// predecessor (PDL): the weights stream while the previous kernel drains.
+// tools/dec_step.py (OPT-30B decode layer, graph replay, L2 flushed): 1 / 2 /
+// 3 / 4 stages -> 115.6 / 112.9 / 112.2 / 112.9 us at M = 1, 138.0 / 136.5 /
+// 135.1 / 135.4 us at M = 16.  DGQ_DEC_PRE overrides it (tools).
+static int decode_pre_stages() {
+  static const int v = [] {
+    const char* e = getenv("DGQ_DEC_PRE");
+    return e ? atoi(e) : 3;
+  }();
+  return v;
+}
+
 // K5d over `count` layers that share the input (one stream-K problem over the
 // concatenation of their weight tiles).  ws: dgq_decode_workspace(total tiles).
 static dgq_status run_decode(const DecodeSub* subs, int count, int g, size_t k_pad, const int8_t* dXq, size_t ldq,
@@ -892,6 +906,7 @@ static dgq_status run_decode(const DecodeSub* subs, int count, int g, size_t k_p
   d.dbg = ((dgq_debug_decode_mode() >> 1) & 0x7F) | ((dgq_debug_decode_mode() >> 12) & 0x1C00) | ((dgq_debug_decode_mode() >> 7) & 0x380);  // tools: mode bits 14-16, 22-24 -> dbg bits 7-9, 10-12
   d.trace = g_dbg_ts;
   d.trace_cta = 0;
+  d.pre_stages = decode_pre_stages();
   DGQ_CUDA(dgq_launch_decode(pl.bn, tmB, d, pl.ctas, pl.pdl != 0, st));
   return DGQ_OK;
 }

@@ -242,14 +242,28 @@ __global__ void __launch_bounds__(dec::kThreads, 1)
         }
         if (btile && !(p.dbg & 8)) tma_load_3d(sB + sl * UPS * kBBytes, &tmB, &full[sl], 0, 0, w.kb);  // tools: bit 3
       };
-      // the first stage's weights do not depend on the previous kernel (PDL);
-      // its Xq tiles do.  Each bulk request occupies the TMA engine for
-      // ~bytes / 32 B per clock, so only one stage goes ahead of the wait.
+      // the first stages' weights do not depend on the previous kernel (PDL);
+      // their Xq tiles do.  Each bulk request occupies the TMA engine for
+      // ~bytes / 32 B per clock, so only p.pre_stages stages go ahead of the wait.
       StageWalk w;
       w.init(u0, nu, KB, ku);
-      issue(w, true, false);
+      const int pre = p.pre_stages < 1 ? 1 : (p.pre_stages > SL ? SL : p.pre_stages);
+      StageWalk w2 = w;
+      int last = 0;  // the last stage whose weights went ahead
+      issue(w2, true, false);
+      for (int i = 1; i < pre; ++i) {
+        w2.next(KB, ku);
+        if (!w2.valid()) break;
+        issue(w2, true, false);
+        last = w2.idx;
+      }
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      issue(w, false, true);
+      // those stages get their Xq tiles; then weights and Xq together
+      for (;;) {
+        issue(w, false, true);
+        if (w.idx == last) break;
+        w.next(KB, ku);
+      }
       for (w.next(KB, ku); w.valid(); w.next(KB, ku)) issue(w, true, true);
       asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }

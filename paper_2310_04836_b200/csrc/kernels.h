@@ -106,6 +106,7 @@ struct DgqDecodeParams {
   int dbg;             // tools only: bit0 skip MMA, bit1 skip unpack, bit2 skip epilogue math
   unsigned long long* trace;  // tools only: [4 roles][1024 units] globaltimer stamps of CTA `trace_cta`
   int trace_cta;
+  int pre_stages;  // stages whose weights are requested before griddepcontrol.wait (>= 1)
 };
 size_t dgq_decode_smem_bytes(int bn, int sl, uint32_t chunk_stride);
 int dgq_decode_stages(int bn);            // units of shared-memory ring (stages x units per stage)
