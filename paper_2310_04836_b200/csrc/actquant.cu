@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 // Without kSparse (a layer with more than T channels k != 1, e.g. random-k
 // tests) the masked lanes divide inline instead (ksm bit masks).
 constexpr int kRing = 8;
-template <int T, int V, bool kF16, bool kDyn, bool kSparse>
+// kExact: the launcher guarantees C8 == T * V (every thread owns exactly V
+// chunks), so the per-chunk `c < C8` guards and their branches compile away.
+template <int T, int V, bool kF16, bool kDyn, bool kSparse, bool kExact = false>
 __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
                                                   const float* __restrict__ kv, const float* __restrict__ rkv,
                                                   const uint8_t* __restrict__ ksm, const int* __restrict__ spec,
@@ -339,13 +341,13 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const int c = threadIdx.x + v * T;
-          r16[v] = c < C8 ? *reinterpret_cast<const uint4*>(buf + c * 16) : make_uint4(0u, 0u, 0u, 0u);
+          r16[v] = (kExact || c < C8) ? *reinterpret_cast<const uint4*>(buf + c * 16) : make_uint4(0u, 0u, 0u, 0u);
         }
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const int c = threadIdx.x + v * T;
-        if (c < C8) {
+        if (kExact || c < C8) {
           if constexpr (kF16) {
             const uint4 raw = kSparse ? r16[kSparse ? v : 0] : *reinterpret_cast<const uint4*>(buf + c * 16);
             if (kSparse || (ksm && !__ldg(ksm + c))) {
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
 #pragma unroll
       for (int v = v0; v < v0 + kG && v < V; ++v) {
         const int c = threadIdx.x + v * T;
-        if (c < C8) {
+        if (kExact || c < C8) {
           raw[v - v0][0] = *reinterpret_cast<const uint4*>(buf + c * 8 * kEsz);
           if constexpr (!kF16) raw[v - v0][1] = *reinterpret_cast<const uint4*>(buf + c * 32 + 16);
         }
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
 #pragma unroll
       for (int v = v0; v < v0 + kG && v < V; ++v) {
         const int c = threadIdx.x + v * T;
-        if (c < C8) {
+        if (kExact || c < C8) {
           float x[8];
           unpack8<kF16>(raw[v - v0], x);
           if constexpr (!kSparse) smooth_sparse(x, ksm ? __ldg(ksm + c) : 0xFFu, kv, rkv, c * 8);
@@ -561,7 +563,12 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
   if (M >= n_sm && C8 <= 16 * 512 && 3 * bufstride <= 220 * 1024) {
     // persistent CTAs of T threads, V <= 16 chunks per thread, `depth` row buffers
     int T = aq_threads();
-    if (!T) T = C8 <= 8 * 256 ? 256 : 512;  // measured (tools/k1_ab.py): <= 8 chunks per thread
+    if (!T) {
+      T = C8 <= 8 * 256 ? 256 : 512;  // measured (tools/k1_ab.py): <= 8 chunks per thread
+      // few special channels (the sparse path) and a row of 7 or 4 chunks per
+      // thread at T = 128: the exact kernel (dense-k rows stay at T = 256)
+      if ((C8 == 7 * 128 || C8 == 4 * 128) && ksm && nspec <= 128) T = 128;
+    }
     while ((C8 + T - 1) / T > 16) T *= 2;
     const int need = (C8 + T - 1) / T;
     int depth = aq_depth();
@@ -570,7 +577,7 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     const size_t smem = depth * bufstride;
 #define DGQ_AQ3_K(T_, V_, F_, D_, S_)                                                                          \
   {                                                                                                             \
-    auto kern = k_actquant3<T_, V_, F_, D_, S_>;                                                                \
+    auto kern = k_actquant3<T_, (V_ < 0 ? -V_ : V_), F_, D_, S_, (V_ < 0)>;                                    \
     { cudaError_t e_ = dgq_allow_smem(kern, smem); if (e_ != cudaSuccess) return e_; }                        \
     int occ = 1;                                                                                                \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, smem);                                        \
@@ -599,6 +606,13 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     if (need <= 12) DGQ_AQ3(T_, 12)                                                                             \
     DGQ_AQ3(T_, 16)                                                                                             \
   }
+    // exact shapes (C8 == T * V): no per-chunk guards, no idle chunk slots
+    // (tools/k1_ab.py, 2048 rows, smoothed k: K = 28672 f16 50.7 -> 43.8 us at
+    // T = 512; K = 7168 f16 16.3 -> 14.4 us, f32 20.2 -> 19.6 us at T = 128)
+    if (T == 128 && C8 == 7 * 128) DGQ_AQ3(128, -7)
+    if (T == 128 && C8 == 4 * 128) DGQ_AQ3(128, -4)
+    if (T == 256 && C8 == 4 * 256) DGQ_AQ3(256, -4)
+    if (T == 512 && C8 == 7 * 512) DGQ_AQ3(512, -7)
     if (T == 128) DGQ_AQ3_V(128)
     if (T == 256) DGQ_AQ3_V(256)
     DGQ_AQ3_V(512)

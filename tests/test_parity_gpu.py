@@ -149,7 +149,11 @@ def test_actq_random(cuda, port, M, K, mode):
 
 @pytest.mark.parametrize("M,K,mode,f16", [(1, 7168, 1, False), (16, 28672, 1, True), (300, 7168, 1, False),
                                           (2048, 7168, 1, False), (512, 28672, 1, True), (200, 4096, 0, False),
-                                          (333, 4096, 0, True), (160, 20000, 0, False)])
+                                          (333, 4096, 0, True), (160, 20000, 0, False),
+                                          # the exact (guard-free) persistent shapes: C8 = 7 x 128, 4 x 128,
+                                          # 4 x 256, 7 x 512 chunks
+                                          (256, 4096, 1, False), (400, 8192, 1, True), (2048, 28672, 1, True),
+                                          (1000, 7168, 1, True)])
 def test_actq_smoothing_vector_with_unit_chunks(cuda, port, M, K, mode, f16):
     # k from the reference's compute_smooth recipe: exactly 1 on ~96 % of the
     # 8-channel chunks (K1 skips their division) and > 1 on the outliers
