@@ -882,17 +882,17 @@ def run_ours(args):
     n_launches = len(layer.k_events) + len(layer.q_events)
     # DRAM traffic of the K5 launches from the committed ncu captures (one
     # `ncu --set full` launch per shape, tools/profile_r02.sh): average bytes per
-    # launch over the step's six linears (q/k/v/out share the q capture)
+    # launch over the step's four K5 launches (the out projection has q's shape)
     traffic, traffic_by = None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r02b.json")
     if os.path.exists(prof) and world == 1:
         try:
             pr = json.load(open(prof))
 
             def _db(k):
                 return (float(pr[k]["dram__bytes_read.sum"]) + float(pr[k]["dram__bytes_write.sum"])) * 1e6
-            traffic_by = {"q/k/v/out": _db("k5p_q"), "fc1": _db("k5p_fc1"), "fc2": _db("k5p_fc2")}
-            traffic = (4 * traffic_by["q/k/v/out"] + traffic_by["fc1"] + traffic_by["fc2"]) / 6
+            traffic_by = {"qkv": _db("k5p_qkv"), "out": _db("k5p_q"), "fc1": _db("k5p_fc1"), "fc2": _db("k5p_fc2")}
+            traffic = sum(traffic_by.values()) / 4
         except Exception:
             traffic, traffic_by = None, None
 

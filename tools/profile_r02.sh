@@ -5,6 +5,8 @@ set -x
 mkdir -p gpurun_out/prof
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-detail --no-cpu > gpurun_out/prof/bench_under_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_dgq_prefill2 -s 2 -c 1 \
+    -o gpurun_out/prof/k5p_qkv python tools/k5_qkv.py 2048 > /dev/null 2>&1
 for shape in "2048 7168 7168 q" "2048 7168 28672 fc1" "2048 28672 7168 fc2"; do
   set -- $shape
   ncu --set full --clock-control none --import-source on -k regex:k_dgq_prefill2 -s 2 -c 1 \

@@ -1,6 +1,6 @@
 """Summarise tools/profile_r02.sh's ncu artifacts into one small JSON (run where
 the .ncu-rep files are; copy the result to profiles/).
-python tools/summarize_r02.py <dir> <out.json>"""
+python tools/summarize_r02.py <dir> <out.json> [launches per step, default 8]"""
 import collections
 import csv
 import io
@@ -24,7 +24,8 @@ for r in rows:
         if x.get("Metric Name") == "gpu__time_duration.sum":
             ks.append((x["Kernel Name"].split("(")[0].replace("void ", ""), x["Grid Size"], float(x["Metric Value"]) / 1e3))
 ours = [k for k in ks if "dgqk::" in k[0]]
-step = ours[-10:]  # the last timed step: 4 K1 + 6 K5
+n_step = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+step = ours[-n_step:]  # the last timed step: 4 K1 + 4 K5 (q/k/v fused into one launch)
 tot = sum(t for *_, t in step)
 agg = collections.OrderedDict()
 for n, g, t in step:
