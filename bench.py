@@ -916,56 +916,61 @@ def run_ours(args):
     # ---- detail: layer ms at seq 512 / 1024, decode (M = 16) weight bandwidth ----------------
     detail = {}
     if not args.no_detail:
-        for M in (512, 1024):
-            t = timed_steps(layer, M, 3, 1, flush, sync_all)
-            tm = max_over_ranks(sum(t)) / 3
-            detail[f"layer_ms_seq{M}"] = tm * 1e3
-            detail[f"tops_seq{M}"] = layer_ops(M) / tm / 1e12
-        detail["layer_ms_seq2048"] = ms_per_step
-        for M in (1, 16):
-            # decode steps are launch-bound from Python: replay the step from a CUDA graph
-            # (single rank) so the number is the GPU's; L2 flushed before every replay
-            tm = decode_step_time(layer, M, flush, sync_all, world)
-            tm = max_over_ranks(tm)
-            wb = layer_weight_bytes(world)
-            detail[f"decode_m{M}_layer_us"] = tm * 1e6
-            detail[f"decode_m{M}_weight_GBps_per_gpu"] = wb / tm / 1e9
-            detail[f"decode_m{M}_hbm_frac"] = wb / tm / 1e9 / hbm_peak
+        try:
+            for M in (512, 1024):
+                t = timed_steps(layer, M, 3, 1, flush, sync_all)
+                tm = max_over_ranks(sum(t)) / 3
+                detail[f"layer_ms_seq{M}"] = tm * 1e3
+                detail[f"tops_seq{M}"] = layer_ops(M) / tm / 1e12
+            detail["layer_ms_seq2048"] = ms_per_step
+            for M in (1, 16):
+                # decode steps are launch-bound from Python: replay the step from a CUDA graph
+                # (single rank) so the number is the GPU's; L2 flushed before every replay
+                tm = decode_step_time(layer, M, flush, sync_all, world)
+                tm = max_over_ranks(tm)
+                wb = layer_weight_bytes(world)
+                detail[f"decode_m{M}_layer_us"] = tm * 1e6
+                detail[f"decode_m{M}_weight_GBps_per_gpu"] = wb / tm / 1e9
+                detail[f"decode_m{M}_hbm_frac"] = wb / tm / 1e9 / hbm_peak
+                if world == 1:
+                    kb = decode_k5_bandwidth(layer, M, flush)
+                    detail[f"decode_m{M}_k5_GBps"] = kb
+                    detail[f"decode_m{M}_k5_hbm_frac"] = {n: v / hbm_peak for n, v in kb.items()}
+                    try:
+                        st = decode_k5_streaming(layer, M, device, world, group)
+                        detail[f"decode_m{M}_k5_streaming"] = {n: dict(v, hbm_frac=v["GBps"] / hbm_peak)
+                                                              for n, v in st.items()}
+                    except Exception as e:  # noqa: BLE001
+                        detail[f"decode_m{M}_k5_streaming"] = {"error": f"{type(e).__name__}: {e}"}
+            detail["k5_tops_by_linear"] = {n: o / t / 1e12 for n, (t, o) in by_name.items()}
+            if traffic_by:
+                alg = {n: k5_bytes(SEQ, K, N // world) for n, K, N in (("out", 7168, 7168), ("fc1", 7168, 28672),
+                                                                         ("fc2", 28672, 7168))}
+                # the fused q/k/v launch reads the shared codes and row scales once
+                alg["qkv"] = 3 * alg["out"] - 2 * (SEQ * 7168 + 4 * SEQ)
+                detail["k5_dram_bytes_by_linear"] = {n: {"ncu_dram_bytes": traffic_by[n], "algorithmic_bytes": alg[n],
+                                                         "ratio": round(traffic_by[n] / alg[n], 2)} for n in alg}
+            detail["k1_GBps"] = k1_b / k1_t / 1e9
+            detail["k1_GBps_by_input"] = {n: x / t / 1e9 for n, (t, x) in k1_by.items()}
+            plans = {n: layer.lin[n].layer.plan(SEQ) for n in ("q", "fc1", "fc2")}
+            detail["plans_seq2048"] = plans
             if world == 1:
-                kb = decode_k5_bandwidth(layer, M, flush)
-                detail[f"decode_m{M}_k5_GBps"] = kb
-                detail[f"decode_m{M}_k5_hbm_frac"] = {n: v / hbm_peak for n, v in kb.items()}
                 try:
-                    st = decode_k5_streaming(layer, M, device, world, group)
-                    detail[f"decode_m{M}_k5_streaming"] = {n: dict(v, hbm_frac=v["GBps"] / hbm_peak)
-                                                          for n, v in st.items()}
+                    detail["comparators"] = comparators(layer, flush)
+                except Exception as e:  # noqa: BLE001  (a library baseline must not sink the bench line)
+                    detail["comparators"] = {"error": f"{type(e).__name__}: {e}"}
+                try:
+                    detail["serving_call_host_buffers"] = serving_call_detail(layer)
                 except Exception as e:  # noqa: BLE001
-                    detail[f"decode_m{M}_k5_streaming"] = {"error": f"{type(e).__name__}: {e}"}
-        detail["k5_tops_by_linear"] = {n: o / t / 1e12 for n, (t, o) in by_name.items()}
-        if traffic_by:
-            alg = {n: k5_bytes(SEQ, K, N // world) for n, K, N in (("q/k/v/out", 7168, 7168), ("fc1", 7168, 28672),
-                                                                     ("fc2", 28672, 7168))}
-            detail["k5_dram_bytes_by_linear"] = {n: {"ncu_dram_bytes": traffic_by[n], "algorithmic_bytes": alg[n],
-                                                     "ratio": round(traffic_by[n] / alg[n], 2)} for n in alg}
-        detail["k1_GBps"] = k1_b / k1_t / 1e9
-        detail["k1_GBps_by_input"] = {n: x / t / 1e9 for n, (t, x) in k1_by.items()}
-        plans = {n: layer.lin[n].layer.plan(SEQ) for n in ("q", "fc1", "fc2")}
-        detail["plans_seq2048"] = plans
-        if world == 1:
-            try:
-                detail["comparators"] = comparators(layer, flush)
-            except Exception as e:  # noqa: BLE001  (a library baseline must not sink the bench line)
-                detail["comparators"] = {"error": f"{type(e).__name__}: {e}"}
-            try:
-                detail["serving_call_host_buffers"] = serving_call_detail(layer)
-            except Exception as e:  # noqa: BLE001
-                detail["serving_call_host_buffers"] = {"error": f"{type(e).__name__}: {e}"}
-            try:
-                detail["configs"] = config_sweeps(device, hbm_peak, i8_peak)
-            except Exception as e:  # noqa: BLE001
-                detail["configs"] = {"error": f"{type(e).__name__}: {e}"}
-        detail["peaks"] = {"hbm_GBps": hbm_peak, "i8_tcgen05_TOPS": i8_tc, "i8_cublaslt_TOPS": i8_cublas,
-                           "i8_2x_bf16_TOPS": i8_proxy}
+                    detail["serving_call_host_buffers"] = {"error": f"{type(e).__name__}: {e}"}
+                try:
+                    detail["configs"] = config_sweeps(device, hbm_peak, i8_peak)
+                except Exception as e:  # noqa: BLE001
+                    detail["configs"] = {"error": f"{type(e).__name__}: {e}"}
+            detail["peaks"] = {"hbm_GBps": hbm_peak, "i8_tcgen05_TOPS": i8_tc, "i8_cublaslt_TOPS": i8_cublas,
+                               "i8_2x_bf16_TOPS": i8_proxy}
+        except Exception as e:  # noqa: BLE001  (a detail probe must never sink the headline line)
+            detail["error"] = f"{type(e).__name__}: {e}"
 
     cpu = None
     if rank == 0 and not args.no_cpu:
