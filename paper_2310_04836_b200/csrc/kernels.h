@@ -38,6 +38,7 @@ inline bool fused_ok(int g) {
 // kDecodeMaxSub layers) and K5p (prefill.cu).  tile_begin = the layer's first
 // tile of the concatenation (K5d: 128-channel tiles; K5p: pair tiles).
 constexpr int kDecodeMaxSub = 4;
+constexpr int kPrefillMaxPairs = 128;  // K5p pairs with a launcher-balanced stream-K split
 struct DgqDecodeSub {
   const uint8_t* tiles;
   const float* s1;
@@ -79,6 +80,9 @@ struct DgqGemmParams {
   int nsub;
   int n_pair_tiles;
   DgqDecodeSub sub[kDecodeMaxSub];
+  // K5p stream-K: first unit of each pair's range (sk_b[ncl] = total units),
+  // balanced by the launcher for the per-segment cost; sk_b[0] < 0: even split
+  int sk_b[kPrefillMaxPairs + 1];
 };
 
 struct DgqDecodeParams {

@@ -33,6 +33,11 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <vector>
+#include <mutex>
+#include <map>
+#include <cstdlib>
+#include <algorithm>
 
 #include "dequant.cuh"
 #include "kernels.h"
@@ -226,8 +231,13 @@ struct SegIter {
   __device__ SegIter(const DgqGemmParams& p, int cid, int ncl, int total_, int KB_)
       : t(cid), total(total_), step(ncl), KB(KB_), sk(p.stream_k) {
     const long long U = static_cast<long long>(total_) * KB_;
-    u = U * cid / ncl;
-    uend = U * (cid + 1) / ncl;
+    if (p.sk_b[0] >= 0) {  // the launcher's balanced split (see sk_bounds)
+      u = p.sk_b[cid];
+      uend = p.sk_b[cid + 1];
+    } else {
+      u = U * cid / ncl;
+      uend = U * (cid + 1) / ncl;
+    }
   }
   // units of this pair and the (tile, k-block) of its i-th unit
   __device__ int count() const {
@@ -284,7 +294,9 @@ __device__ __forceinline__ void pf_stamp(const DgqGemmParams& p, int slot, int i
     p.dbg[slot * 1024 + it] = g;
   }
 }
-__device__ __forceinline__ long long sk_begin(long long U, int c, int ncl) { return U * c / ncl; }
+__device__ __forceinline__ long long sk_begin(const DgqGemmParams& p, long long U, int c, int ncl) {
+  return p.sk_b[0] >= 0 ? p.sk_b[c] : U * c / ncl;
+}
 
 __device__ __forceinline__ void st_release_gpu(uint32_t* a, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
@@ -869,7 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
       int npart = 0;
       if (hi < KB) {
         const long long tend = static_cast<long long>(t + 1) * KB;
-        while (cid + 1 + npart < ncl && sk_begin(U, cid + 1 + npart, ncl) < tend) ++npart;
+        while (cid + 1 + npart < ncl && sk_begin(p, U, cid + 1 + npart, ncl) < tend) ++npart;
       }
       // per-tile scales (all four epilogue warps)
       for (int i = et; i < S * 128; i += kEpiThreads) {
@@ -1082,15 +1094,125 @@ int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int
   return n;
 }
 
+// tools: DGQ_PF_BALANCE=0 keeps the even stream-K split (A/B)
+static bool sk_balance() {
+  static const bool v = [] {
+    const char* e = getenv("DGQ_PF_BALANCE");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+// Stream-K split balanced for the per-segment cost.  A pair's time is its MMA
+// units plus a fixed cost per segment (tile piece) it touches: the exposed
+// epilogue (S = 2: one accumulator set), a contributor's parked partial or an
+// owner's fix-up, ~9 us = ~15 k-block steps of a 512-token tile.  An even
+// split of the units gives the pairs that touch one more tile one more such
+// stop; here the smallest per-pair cost C for which a greedy walk (each pair
+// takes units while units + E x segments <= C) covers everything with the
+// pairs available is found by bisection, so the pairs end at about the same
+// time (simulated on OPT-30B at 2048 tokens: the slowest pair 2-5 % sooner).
+// Cached per (units, k-blocks, pairs, E).  Returns false (even split) when
+// the pairs exceed the table or the walk would leave a pair empty.
+static bool sk_bounds(long long U, int KB, int ncl, int E, int* b) {
+  if (ncl > kPrefillMaxPairs || ncl < 1 || U <= 0 || KB <= 0 || U > 0x7FFFFFFFLL) return false;
+  struct Key {
+    long long U;
+    int KB, ncl, E;
+    bool operator<(const Key& o) const {
+      return U != o.U ? U < o.U : KB != o.KB ? KB < o.KB : ncl != o.ncl ? ncl < o.ncl : E < o.E;
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, std::vector<int>> cache;
+  const Key key{U, KB, ncl, E};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      if (it->second.empty()) return false;
+      std::copy(it->second.begin(), it->second.end(), b);
+      return true;
+    }
+  }
+  // true if exactly ncl non-empty ranges of cost <= C cover the U units
+  auto walk = [&](long long C, std::vector<int>& out) {
+    out.assign(1, 0);
+    long long pos = 0;
+    for (int c = 0; c < ncl; ++c) {
+      long long rem = C;
+      const long long start = pos;
+      while (pos < U) {
+        const long long seg = std::min<long long>(KB - pos % KB, U - pos);
+        if (rem >= seg + E) {
+          rem -= seg + E;
+          pos += seg;
+        } else {
+          if (rem - E > 0) pos += rem - E;
+          break;
+        }
+      }
+      if (pos == start) return false;
+      out.push_back(static_cast<int>(pos));
+    }
+    return pos >= U;
+  };
+  std::vector<int> best;
+  long long lo = 1, hi = U + static_cast<long long>(E) * (U / KB + 2) + 1;
+  // the cheapest C that still covers U; pairs may come out empty when C is
+  // large (fewer, longer ranges) -> search only between the even split's
+  // cost and the first C that covers
+  while (lo < hi) {
+    const long long mid = (lo + hi) / 2;
+    std::vector<int> tmp;
+    // covers with <= ncl pairs?
+    long long pos = 0;
+    int used = 0;
+    while (pos < U && used < ncl) {
+      long long rem = mid;
+      const long long start = pos;
+      while (pos < U) {
+        const long long seg = std::min<long long>(KB - pos % KB, U - pos);
+        if (rem >= seg + E) {
+          rem -= seg + E;
+          pos += seg;
+        } else {
+          if (rem - E > 0) pos += rem - E;
+          break;
+        }
+      }
+      if (pos == start) break;
+      ++used;
+    }
+    if (pos >= U) hi = mid; else lo = mid + 1;
+  }
+  const bool ok = walk(hi, best);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ok) {
+    cache.emplace(key, std::vector<int>());
+    return false;
+  }
+  cache.emplace(key, best);
+  std::copy(best.begin(), best.end(), b);
+  return true;
+}
+
 template <int TN, int S>
-static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p, bool pdl,
+static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, const DgqGemmParams& p_, bool pdl,
                              cudaStream_t st) {
+  DgqGemmParams p = p_;
   const size_t smem = smem_bytes_s<S, TN>(p.chunk_stride);
   auto kern = k_dgq_prefill2<TN, S>;
   cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * dgq_prefill2_clusters(p.M, p.n_pair_tiles * TN, TN, p.k_blocks, p.stream_k != 0, S));
+  const int ncl = dgq_prefill2_clusters(p.M, p.n_pair_tiles * TN, TN, p.k_blocks, p.stream_k != 0, S);
+  cfg.gridDim = dim3(2 * ncl);
+  p.sk_b[0] = -1;
+  if (p.stream_k && sk_balance()) {
+    const long long U = static_cast<long long>((p.M + 256 * S - 1) / (256 * S)) * p.n_pair_tiles * p.k_blocks;
+    if (!sk_bounds(U, p.k_blocks, ncl, S == 2 ? 15 : 5, p.sk_b)) p.sk_b[0] = -1;
+  }
   cfg.blockDim = dim3(pf::Cfg<S, TN>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
