@@ -59,13 +59,18 @@ namespace pf {
 template <int S, int TN = 256>
 struct Cfg {
   static constexpr int kSA = S == 1 ? 5 : 3;        // Xq stages (S tiles each, released by the MMA)
-  static constexpr int kSC = S == 1 ? 7 : 5;        // packed-chunk stages (released by the dequantisers)
+#ifndef DGQ_PF_EPIW2
+#define DGQ_PF_EPIW2 12  // epilogue warps at S = 2 (8: two per TMEM lane quadrant, 4 KB staging each)
+#endif
+  // S == 2 exposes the epilogue (one accumulator set): three warps per TMEM
+  // lane quadrant split the channels, with 2 KB staging buffers (64-byte row
+  // segments) and one packed-chunk stage fewer to fit
+  static constexpr int kEpiWarps = S == 1 ? 4 : DGQ_PF_EPIW2;
+  static constexpr uint32_t kStagingPerWarp = (S == 2 && kEpiWarps > 8) ? 2048 : 4096;
+  static constexpr int kSC = S == 1 ? 7 : (kEpiWarps > 8 ? 4 : 5);  // packed-chunk stages (released by the dequantisers)
   static constexpr int kSB = S == 1 ? 4 : 3;        // dequantised weight-tile slots (> dequant groups)
   static constexpr int kDqGroups = S == 1 ? 3 : 2;  // groups of four dequant warps, alternate k-blocks
   static constexpr int kEpiWarp0 = 4 + 4 * kDqGroups;  // first epilogue warp
-  // S == 2 exposes the epilogue (one accumulator set): two warps per TMEM lane
-  // quadrant split the channels
-  static constexpr int kEpiWarps = S == 1 ? 4 : 8;
   static constexpr int kXWarp = kEpiWarp0 + kEpiWarps;  // second Xq-tile producer warp
   static constexpr int kThreads = 32 * (kXWarp + 1);
   // accumulator sets in TMEM (TN * S columns each): two whenever they fit, so a
@@ -74,7 +79,6 @@ struct Cfg {
 };
 constexpr uint32_t kATile = 128 * 128;   // 128 token rows x 128 k (bytes)
 constexpr uint32_t kBTile = 128 * 128;   // 128 channel rows x 128 k
-constexpr uint32_t kStagingPerWarp = 4096;  // epilogue: one 4 KB staging buffer per epilogue warp
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -319,7 +323,7 @@ __device__ __forceinline__ size_t part_off(int c16, int v, int row) {
 // whole 128-byte row segments (a lane-per-row 16-byte store touched 32 lines
 // per instruction; tools/pf_trace.py measured an 11 us epilogue that way, and
 // a TMA store per 64 columns serialises on its issue latency).
-template <int TN, bool kF16, bool kFlush>
+template <int TN, bool kF16, bool kFlush, int kRowB>
 __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, const DgqDecodeSub& d, uint32_t tbase, float rsm,
                                            const float* s_s1, const float* s_bias, uint8_t* stg, int mrow0, int nbase,
                                            int cbeg, int cend) {
@@ -327,10 +331,14 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, const DgqDeco
   // template variant unrolled here cost instruction-cache misses (the kernel's
   // SASS reached 350 KB and the exposed epilogue ran at ~1/6 of its issue rate)
   const bool kF16Mode = p.fp16_mode != 0, kBias = d.bias != nullptr;
-  constexpr int kCB = kF16 ? 64 : 32;  // columns per 128-byte row segment
+  // the warp's staging buffer holds 32 rows x kRowB bytes (128 or 64): the
+  // 16-byte chunks of a row are XOR-swizzled so the row-per-lane writes and the
+  // transposed reads hit distinct banks
+  constexpr int kCB = kRowB / (kF16 ? 2 : 4);  // columns per row segment
+  constexpr int kNC = kRowB / 16;               // 16-byte chunks per row segment
   const uint32_t lane = lane_id();
-  uint8_t* myrow = stg + lane * 128;
-  const uint32_t sw = lane & 7;
+  uint8_t* myrow = stg + lane * kRowB;
+  const uint32_t sw = kNC == 8 ? (lane & 7) : ((lane >> 1) & 3);
 #pragma unroll 1
   for (int c0 = cbeg; c0 < cend; c0 += kCB) {
     if (nbase + c0 >= d.N) break;
@@ -416,8 +424,9 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, const DgqDeco
     }
     __syncwarp();
     if (p.dbg_flags & 2) continue;  // tools (mode bit 19): no global stores
-    // 8 passes x (4 rows x 8 lanes x 16 bytes)
-    const int ch = static_cast<int>(lane & 7);                 // 16-byte chunk of the row segment
+    // 32 / kRPP passes x (kRPP rows x kNC lanes x 16 bytes)
+    constexpr int kRPP = 32 / kNC;                              // rows per pass
+    const int ch = static_cast<int>(lane % kNC);                // 16-byte chunk of the row segment
     const int n = nbase + c0 + ch * (kF16 ? 8 : 4);            // first output column of the chunk
     constexpr int kPer = kF16 ? 8 : 4;                         // outputs per chunk
     uint8_t* const out0 = static_cast<uint8_t*>(d.out) + (static_cast<size_t>(mrow0) * d.ldy + n) * (kF16 ? 2 : 4);
@@ -425,17 +434,19 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, const DgqDeco
     if (mrow0 + 32 <= p.M && nbase + c0 + kCB <= d.N) {
       // interior block: no per-store bounds checks (branches cost the exposed epilogue)
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int row = it * 4 + static_cast<int>(lane >> 3);
-        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
+      for (int it = 0; it < 32 / kRPP; ++it) {
+        const int row = it * kRPP + static_cast<int>(lane / kNC);
+        const int rsw = kNC == 8 ? (row & 7) : ((row >> 1) & 3);
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * kRowB + ((ch ^ rsw) << 4));
         *reinterpret_cast<uint4*>(out0 + row * row_bytes) = v;
       }
     } else {
 #pragma unroll 1
-      for (int it = 0; it < 8; ++it) {
-        const int row = it * 4 + static_cast<int>(lane >> 3);
+      for (int it = 0; it < 32 / kRPP; ++it) {
+        const int row = it * kRPP + static_cast<int>(lane / kNC);
         const int m = mrow0 + row;
-        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 128 + ((ch ^ (row & 7)) << 4));
+        const int rsw = kNC == 8 ? (row & 7) : ((row >> 1) & 3);
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + row * kRowB + ((ch ^ rsw) << 4));
         if (m < p.M) {
           uint8_t* dst = out0 + row * row_bytes;
           if (n + kPer <= d.N) {
@@ -528,6 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
   constexpr int kSA = C::kSA, kSC = C::kSC, kSB = C::kSB, kDqGroups = C::kDqGroups;
   constexpr int kEpiWarp0 = C::kEpiWarp0, kXWarp = C::kXWarp, kNAcc = C::kNAcc, kEpiWarps = C::kEpiWarps;
   constexpr int kEpiThreads = 32 * kEpiWarps;
+  constexpr uint32_t kStagingPerWarp = C::kStagingPerWarp;
   constexpr uint32_t kStaging = kEpiWarps * kStagingPerWarp;
   constexpr uint32_t kAStage = S * kATile;  // one Xq stage: S tiles of 128 token rows
   constexpr uint32_t kIdesc = idesc_i8(256, TN);
@@ -824,8 +836,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
     const int et = threadIdx.x - 32 * kEpiWarp0;     // 0 .. kEpiThreads-1
     const uint32_t q = warp & 3;                     // TMEM lane quadrant
     const int e = static_cast<int>(q * 32 + lane);   // token row of this CTA's D
-    constexpr int kCols = TN / (kEpiWarps / 4);       // channels per warp
-    const int cbeg = ((warp - kEpiWarp0) >> 2) * kCols, cend = cbeg + kCols;
+    // channels of this warp: the quadrant's kEpiWarps / 4 warps split the TN
+    // columns in 32-column units (three warps: 2 / 3 / 3 units of 8)
+    constexpr int kPerQ = kEpiWarps / 4, kUnits = TN / 32;
+    const int jq = static_cast<int>(warp - kEpiWarp0) >> 2;
+    const int cbeg = (jq * kUnits / kPerQ) * 32, cend = ((jq + 1) * kUnits / kPerQ) * 32;
     const uint32_t tempty_leader = mapa(tempty, 0);
     uint8_t* stg0 = sStg + (warp - kEpiWarp0) * kStagingPerWarp;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // row scales from K1
@@ -957,11 +972,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
             const bool safe = !d.bias && !p.fp16_mode && __fmul_rn(rsm, s1min) >= 0x1p-24f;
             if (p.out_f16) {
               if (__all_sync(0xffffffffu, safe))
-                epi_direct<TN, true, false>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+                epi_direct<TN, true, false, kStagingPerWarp / 32>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
               else
-                epi_direct<TN, true, true>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+                epi_direct<TN, true, true, kStagingPerWarp / 32>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
             } else {
-              epi_direct<TN, false, true>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
+              epi_direct<TN, false, true, kStagingPerWarp / 32>(p, d, tbase, rsm, s_s1, s_bias, stg0, m0 + q * 32, n0, cbeg, cend);
             }
           }
         } else if (S == 1 && p.tma_out && !p.acc_out) {
@@ -1038,7 +1053,7 @@ template <int S, int TN = 256>
 static size_t smem_bytes_s(uint32_t chunk_stride) {
   using C = pf::Cfg<S, TN>;
   return 1024 + static_cast<size_t>(C::kSA) * S * pf::kATile + C::kSC * chunk_stride + C::kSB * pf::kBTile +
-         C::kEpiWarps * pf::kStagingPerWarp + (2 * C::kSA + 2 * C::kSC + 2 * C::kSB + 5) * 8 + 32 +
+         C::kEpiWarps * C::kStagingPerWarp + (2 * C::kSA + 2 * C::kSC + 2 * C::kSB + 5) * 8 + 32 +
          (128 * S + 256 + 256) * 4;
 }
 

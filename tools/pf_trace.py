@@ -44,6 +44,8 @@ d = np.diff(b[0][:n]) / 1e3
 big = [(i + 1, round(float(d[i]), 2)) for i in range(len(d)) if d[i] > 1.0]
 print(f"MMA of CTA 0: first {r(b[0][0]):.2f} last {r(b[0][n - 1]):.2f} us; gaps > 1 us at k-block (index, us): {big[:12]}")
 print(f"MMA period median {np.median(d):.3f} us over {n} k-blocks")
+print("MMA issue around the first tile boundary (k-block: us):",
+      [(i, round(r(b[0][i]), 2)) for i in range(50, 60) if i < n])
 lat = lambda a, c: np.median((b[c][:n] - b[a][:n]) / 1e3)  # noqa: E731
 print(f"median: issue->full {lat(1, 2):.3f}  full->bempty {lat(2, 3):.3f}  bempty->done {lat(3, 4):.3f}  "
       f"done->mma {lat(4, 0):.3f}  issue->mma {lat(1, 0):.3f} us")
