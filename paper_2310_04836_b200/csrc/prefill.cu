@@ -1092,7 +1092,11 @@ int dgq_prefill2_clusters(int M, int N, int tn, int k_blocks, bool stream_k, int
   const long long tiles = static_cast<long long>((M + 256 * sub - 1) / (256 * sub)) * ((N + tn - 1) / tn);
   const long long work = stream_k ? tiles * k_blocks : tiles;
   int n = static_cast<int>(work < pairs ? work : pairs);
-  if (stream_k && tiles > 0) {
+  static const bool dp_switch = [] {  // tools: DGQ_PF_DP=0 always splits stream-K over every pair
+    const char* e = getenv("DGQ_PF_DP");
+    return !(e && atoi(e) == 0);
+  }();
+  if (stream_k && tiles > 0 && dp_switch) {
     // Whole tiles per pair when that is cheaper than splitting them: a split
     // tile costs its owner a wait + fix-up and its contributors a partial
     // store (~6 us per piece, tools/decode_sweep.py --cap: 4096^2 at M = 1024
