@@ -1128,13 +1128,15 @@ static bool sk_balance() {
 // owner's fix-up, ~9 us = ~15 k-block steps of a 512-token tile.  An even
 // split of the units gives the pairs that touch one more tile one more such
 // stop; here the smallest per-pair cost C for which a greedy walk (each pair
-// takes units while units + E x segments <= C) covers everything with the
-// pairs available is found by bisection, so the pairs end at about the same
-// time (simulated on OPT-30B at 2048 tokens: the slowest pair 2-5 % sooner).
-// Cached per (units, k-blocks, pairs, E).  Returns false (even split) when
-// the pairs exceed the table or the walk would leave a pair empty.
-static bool sk_bounds(long long U, int KB, int ncl, int E, int* b) {
-  if (ncl > kPrefillMaxPairs || ncl < 1 || U <= 0 || KB <= 0 || U > 0x7FFFFFFFLL) return false;
+// takes units while units + E x segments <= C) covers everything with at most
+// `ncl` pairs is found by bisection, so the pairs end at about the same time
+// (simulated on OPT-30B at 2048 tokens: the slowest pair 2-5 % sooner).  The
+// walk may need fewer pairs than available: the launch then uses that many
+// (every range non-empty, which the owners' contributor count relies on).
+// Returns the pairs used (b[0..used] = range starts, b[used] = U), or 0 for
+// the even split (more pairs than the table holds).  Cached per (U, KB, ncl, E).
+static int sk_bounds(long long U, int KB, int ncl, int E, int* b) {
+  if (ncl > kPrefillMaxPairs || ncl < 1 || U <= 0 || KB <= 0 || U > 0x7FFFFFFFLL || E < 0) return 0;
   struct Key {
     long long U;
     int KB, ncl, E;
@@ -1149,16 +1151,15 @@ static bool sk_bounds(long long U, int KB, int ncl, int E, int* b) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) {
-      if (it->second.empty()) return false;
       std::copy(it->second.begin(), it->second.end(), b);
-      return true;
+      return static_cast<int>(it->second.size()) - 1;
     }
   }
-  // true if exactly ncl non-empty ranges of cost <= C cover the U units
-  auto walk = [&](long long C, std::vector<int>& out) {
-    out.assign(1, 0);
+  // greedy ranges of cost <= C; true when they cover U with at most ncl pairs
+  auto walk = [&](long long C, std::vector<int>* out) {
+    if (out) out->assign(1, 0);
     long long pos = 0;
-    for (int c = 0; c < ncl; ++c) {
+    for (int c = 0; c < ncl && pos < U; ++c) {
       long long rem = C;
       const long long start = pos;
       while (pos < U) {
@@ -1171,49 +1172,27 @@ static bool sk_bounds(long long U, int KB, int ncl, int E, int* b) {
           break;
         }
       }
-      if (pos == start) return false;
-      out.push_back(static_cast<int>(pos));
+      if (pos == start) return false;  // C below one unit + E
+      if (out) out->push_back(static_cast<int>(pos));
     }
     return pos >= U;
   };
-  std::vector<int> best;
-  long long lo = 1, hi = U + static_cast<long long>(E) * (U / KB + 2) + 1;
-  // the cheapest C that still covers U; pairs may come out empty when C is
-  // large (fewer, longer ranges) -> search only between the even split's
-  // cost and the first C that covers
+  long long lo = 1, hi = U + static_cast<long long>(E) * (U / KB + 2) + 1;  // one pair takes everything
   while (lo < hi) {
-    const long long mid = (lo + hi) / 2;
-    std::vector<int> tmp;
-    // covers with <= ncl pairs?
-    long long pos = 0;
-    int used = 0;
-    while (pos < U && used < ncl) {
-      long long rem = mid;
-      const long long start = pos;
-      while (pos < U) {
-        const long long seg = std::min<long long>(KB - pos % KB, U - pos);
-        if (rem >= seg + E) {
-          rem -= seg + E;
-          pos += seg;
-        } else {
-          if (rem - E > 0) pos += rem - E;
-          break;
-        }
-      }
-      if (pos == start) break;
-      ++used;
-    }
-    if (pos >= U) hi = mid; else lo = mid + 1;
+    const long long mid = lo + (hi - lo) / 2;
+    if (walk(mid, nullptr)) hi = mid; else lo = mid + 1;
   }
-  const bool ok = walk(hi, best);
+  std::vector<int> best;
+  walk(hi, &best);
   std::lock_guard<std::mutex> lk(mu);
-  if (!ok) {
-    cache.emplace(key, std::vector<int>());
-    return false;
-  }
   cache.emplace(key, best);
   std::copy(best.begin(), best.end(), b);
-  return true;
+  return static_cast<int>(best.size()) - 1;
+}
+
+// not in the public header: the balanced split for tools / host-side tests
+extern "C" int dgq_debug_sk_bounds(long long U, int KB, int ncl, int E, int* b) {
+  return sk_bounds(U, KB, ncl, E, b);
 }
 
 template <int TN, int S>
@@ -1225,13 +1204,14 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
   cudaError_t e = dgq_allow_smem(kern, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  const int ncl = dgq_prefill2_clusters(p.M, p.n_pair_tiles * TN, TN, p.k_blocks, p.stream_k != 0, S);
-  cfg.gridDim = dim3(2 * ncl);
+  int ncl = dgq_prefill2_clusters(p.M, p.n_pair_tiles * TN, TN, p.k_blocks, p.stream_k != 0, S);
   p.sk_b[0] = -1;
   if (p.stream_k && sk_balance()) {
     const long long U = static_cast<long long>((p.M + 256 * S - 1) / (256 * S)) * p.n_pair_tiles * p.k_blocks;
-    if (!sk_bounds(U, p.k_blocks, ncl, S == 2 ? 15 : 5, p.sk_b)) p.sk_b[0] = -1;
+    const int used = sk_bounds(U, p.k_blocks, ncl, S == 2 ? 15 : 5, p.sk_b);
+    if (used > 0) ncl = used; else p.sk_b[0] = -1;
   }
+  cfg.gridDim = dim3(2 * ncl);
   cfg.blockDim = dim3(pf::Cfg<S, TN>::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

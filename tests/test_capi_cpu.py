@@ -134,3 +134,38 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         dgq.quantize_activations(np.zeros((1, 8), np.float32), dgq.random_layer(8, 2, 8, 1))
+
+
+def _even_cost(b, KB, E):
+    out = []
+    for c in range(len(b) - 1):
+        pos, segs = b[c], 0
+        while pos < b[c + 1]:
+            pos = min((pos // KB + 1) * KB, b[c + 1])
+            segs += 1
+        out.append(b[c + 1] - b[c] + E * segs)
+    return out
+
+
+@pytest.mark.parametrize("tiles,KB,ncl,E", [(336, 56, 74, 15), (112, 56, 74, 15), (448, 56, 74, 15),
+                                            (112, 224, 74, 15), (84, 56, 74, 15), (56, 56, 74, 5),
+                                            (7, 3, 5, 2), (1000, 8, 128, 15)])
+def test_stream_k_balanced_split(tiles, KB, ncl, E):
+    # the K5p launcher's stream-K ranges (csrc/prefill.cu sk_bounds): contiguous,
+    # non-empty, covering every (tile, k-block) unit, and no pair costlier
+    # (units + E x segments) than under the even split
+    import ctypes as C
+
+    L = dgq.lib()
+    f = L.dgq_debug_sk_bounds
+    f.argtypes = [C.c_longlong, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
+    U = tiles * KB
+    b = (C.c_int * (ncl + 1))()
+    used = f(U, KB, ncl, E, b)
+    assert 1 <= used <= ncl  # the launch uses this many pairs
+    b = list(b)[:used + 1]
+    assert b[0] == 0 and b[-1] == U
+    assert all(b[c] < b[c + 1] for c in range(used))
+    even = [U * c // ncl for c in range(ncl + 1)]
+    assert max(_even_cost(b, KB, E)) <= max(_even_cost(even, KB, E))
+    assert f(U, KB, ncl, E, (C.c_int * (ncl + 1))()) == used  # cached
