@@ -16,5 +16,5 @@ layer.x.copy_(torch.from_numpy(bench._synth_x(64, 7168)))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for M in Ms:
     ts = [bench.decode_step_time(layer, M, flush, torch.cuda.synchronize, 1, reps=20) for _ in range(3)]
-    print(f"pre={os.environ.get('DGQ_DEC_PRE', '1')} M={M}: {min(ts) * 1e6:.1f} us (runs {[round(t * 1e6, 1) for t in ts]})",
+    print(f"pre={os.environ.get('DGQ_DEC_PRE', 'default')} M={M}: {min(ts) * 1e6:.1f} us (runs {[round(t * 1e6, 1) for t in ts]})",
           flush=True)
