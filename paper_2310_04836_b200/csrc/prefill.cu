@@ -113,6 +113,25 @@ __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
 __device__ __forceinline__ void arrive_remote_relaxed(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+#ifndef DGQ_PF_TEMPTY_RELAXED
+#define DGQ_PF_TEMPTY_RELAXED 1  // tools: 0 = release.cluster arrive on tempty (A/B)
+#endif
+// "This warp has drained its accumulator rows" to the leader's tempty: the
+// TMEM reads are ordered by tcgen05.fence::before_thread_sync (issued by the
+// caller, after tcgen05.wait::ld), the MMA issuer's acquire wait and its
+// tcgen05.fence::after_thread_sync.  A release arrive at cluster scope would
+// also wait for this warp's ~10 KB of output stores to be performed cluster-
+// wide (~0.8 us of the tile-boundary stop, tools/pf_trace.py): the release
+// here is restricted to shared::cta (nothing in shared memory is published)
+// and the arrive is relaxed, so the stores drain while the next tile's MMAs run.
+__device__ __forceinline__ void arrive_tmem_drained(uint32_t cluster_addr) {
+#if DGQ_PF_TEMPTY_RELAXED
+  asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
+}
 // Barriers completed by arrivals from the PEER CTA are polled with test_wait:
 // a suspended try_wait is not woken promptly by a remote (DSMEM) arrival and
 // sleeps out its time limit (~1000 cycles per k-block, measured).
@@ -132,6 +151,9 @@ __device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t parity)
 #endif
 #ifndef DGQ_PF_RELAXED_READY
 #define DGQ_PF_RELAXED_READY 0  // tools: 1 drops the release fence before the ready arrive (A/B of its cost)
+#endif
+#ifndef DGQ_PF_TSLEEP
+#define DGQ_PF_TSLEEP 128  // ns the MMA issuer sleeps between polls of tempty (tools: A/B)
 #endif
 #ifndef DGQ_PF_BACKOFF
 #define DGQ_PF_BACKOFF 0
@@ -716,7 +738,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
            // sharing its SMSP (the epilogue is exposed when S == 2)
           long long n = 0;
           while (!try_wait_cluster(&tempty[acc], ((tl / kNAcc) & 1) ^ 1)) {
-            __nanosleep(128);
+#if DGQ_PF_TSLEEP > 0
+            __nanosleep(DGQ_PF_TSLEEP);
+#endif
             watchdog(n, 2, 0);
           }
         }
@@ -889,7 +913,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
         named_bar(2, kEpiThreads);
         if (et == 0) st_release_gpu(p.counters + cid * 2 + rank, 1u);
         __syncwarp();
-        if (lane == 0) arrive_remote(tempty_leader + acc * 8);
+        if (lane == 0) arrive_tmem_drained(tempty_leader + acc * 8);
         continue;
       }
       // owner of a split tile: the pairs after this one whose ranges start inside it
@@ -1024,7 +1048,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pf::Cfg<S, TN>::kThr
       tc_fence_before();
       __syncwarp();
       if (et == 0 && tl < 8) pf_stamp(p, 9, 2 * tl + 1);
-      if (lane == 0) arrive_remote(tempty_leader + acc * 8);  // the leader's tempty[acc]
+      if (p.dbg && lane == 0 && tl == 0 && blockIdx.x < 2) {  // tools/pf_trace.py: per-warp drain end, first segment
+        uint64_t g;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+        p.dbg[10 * 1024 + blockIdx.x * 32 + warp] = g;
+      }
+      if (lane == 0) arrive_tmem_drained(tempty_leader + acc * 8);  // the leader's tempty[acc]
       named_bar(2, kEpiThreads);  // scales of the next tile are rewritten
     }
     if (lane == 0) bulk_wait_all();

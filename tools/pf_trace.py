@@ -19,7 +19,7 @@ CL = dgq.CudaLayer(L, validate=False)
 x = torch.randn(M, K, device="cuda") * 3
 codes, rs = CL.quantize_act(x)
 out = torch.empty(M, N, dtype=torch.float16, device="cuda")
-buf = torch.zeros(10 * 1024, dtype=torch.int64, device="cuda")
+buf = torch.zeros(11 * 1024, dtype=torch.int64, device="cuda")
 lib = dgq.lib()
 lib.dgq_debug_set_timestamps.argtypes = [C.c_void_p]
 lib.dgq_debug_set_decode.argtypes = [C.c_int]
@@ -31,12 +31,12 @@ lib.dgq_debug_set_timestamps(C.c_void_p(buf.data_ptr()))
 CL.linear(codes, rs, out=out)
 torch.cuda.synchronize()
 lib.dgq_debug_set_timestamps(None)
-b = buf.view(10, 1024).cpu().numpy().astype(np.float64)
+b = buf.view(11, 1024).cpu().numpy().astype(np.float64)
 n = int((b[0] > 0).sum())
 t0 = b[:5, :n][b[:5, :n] > 0].min()
 r = lambda v: (v - t0) / 1e3 if v > 0 else float("nan")  # noqa: E731
 print(" kb | issue   full  bempty  dq-done | mma    | A-issue  loop#")
-for i in list(range(20, 30)):
+for i in list(range(20, 24)) + list(range(53, 61)):
     if i < n:
         print(f"{i:3d} | {r(b[1][i]):6.2f} {r(b[2][i]):6.2f} {r(b[3][i]):6.2f} {r(b[4][i]):6.2f} | {r(b[0][i]):6.2f} | "
               f"{r(b[5][i]):6.2f} {int(b[6][i]) if b[6][i] else 0:8d}")
@@ -51,6 +51,10 @@ print(f"median: issue->full {lat(1, 2):.3f}  full->bempty {lat(2, 3):.3f}  bempt
       f"done->mma {lat(4, 0):.3f}  issue->mma {lat(1, 0):.3f} us")
 ep = [(round(r(b[9][2 * i]), 2), round(r(b[9][2 * i + 1]), 2)) for i in range(8) if b[9][2 * i] > 0]
 print("CTA 0 epilogues (start, end) us:", ep)
+for c in range(2):
+    ends = [(w, round(r(b[10][c * 32 + w]), 2)) for w in range(32) if b[10][c * 32 + w] > 0]
+    if ends:
+        print(f"CTA {c} first-segment drain end per epilogue warp (warp, us):", ends)
 print("CTA 0 second-pass starts (dbg 8):", [[round(r(b[9][640 + 4 * i + j]), 2) for j in range(2)] for i in range(4) if b[9][640 + 4 * i] > 0])
 print("CTA 0 epilogue sub-tile starts / end:", [[round(r(b[9][512 + 4 * i + j]), 2) for j in range(3)] for i in range(4) if b[9][512 + 4 * i] > 0])
 st, en = b[7], b[8]
