@@ -19,22 +19,40 @@
 #include "ptx.cuh"
 using namespace dgqk;
 
-template <int W, int V>
-__global__ void __launch_bounds__(W * 32, 1) k_drain(__half* __restrict__ out, const float* __restrict__ s1g,
-                                                    unsigned long long* cyc, int reps) {
+template <int W, int V, int EX = 0>
+__global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__ out, const float* __restrict__ s1g,
+                                                    unsigned long long* cyc, int reps, int ldy_ = 512) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t stop;
   __shared__ __align__(16) float s_s1[512];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, jq = warp >> 2;
   constexpr int kPerQ = W / 4, kUnits = 8;  // 32-column units per 256-column sub-tile
   const int cbeg = (jq * kUnits / kPerQ) * 32, cend = ((jq + 1) * kUnits / kPerQ) * 32;
   for (int i = threadIdx.x; i < 512; i += blockDim.x) s_s1[i] = s1g[i & 255];
+  if (threadIdx.x == 0) {
+    mbar_init(&stop, W);
+    fence_mbar_init();
+  }
   if (warp == 0) tmem_alloc<512>(&tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  if (warp >= W) {  // EX warps waiting on an mbarrier during every drain (the kernel's idle roles)
+    tc_fence_before();
+    __syncthreads();  // the fill barrier
+    for (int rep = 0; rep < reps; ++rep) {
+      __syncthreads();
+      while (!mbar_try_wait(&stop, rep & 1)) {
+      }
+      __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    return;
+  }
   const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
   // fill this warp's share of both sub-tiles
   for (int sub = 0; sub < 2; ++sub)
@@ -52,7 +70,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_drain(__half* __restrict__ out, c
   uint8_t* myrow = stg + lane * 64;
   const uint32_t sw = (lane >> 1) & 3;
   const float rsm = 0.0123f + lane * 1e-4f;
-  const size_t ldy = 512;
+  const size_t ldy = ldy_;
   unsigned long long total = 0;
   for (int rep = 0; rep < reps; ++rep) {
     __syncthreads();
@@ -143,7 +161,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_drain(__half* __restrict__ out, c
       }
       if (V == 3) tmem_ld_wait();
     }
+    if (lane == 0) mbar_arrive(&stop);
     __syncthreads();
+    if (rep == 0 && threadIdx.x == 0) cyc[148 + blockIdx.x] = clock64() - t0;  // first (cold) drain
     total += clock64() - t0;
   }
   if (threadIdx.x == 0) cyc[blockIdx.x] = total / reps;
@@ -246,35 +266,37 @@ static void run128(__half* out, const float* s1, unsigned long long* cyc) {
   printf("W=%2d 128-byte rows: %7.0f cycles per 128x512 drain = %.2f us at 1.93 GHz\n", W, m / 148, m / 148 / 1930.0);
 }
 
-template <int W, int V>
-static void run(__half* out, const float* s1, unsigned long long* cyc, int ctas = 148) {
-  auto k = k_drain<W, V>;
+template <int W, int V, int EX = 0>
+static void run(__half* out, const float* s1, unsigned long long* cyc, int ctas = 148, int ldy = 512) {
+  auto k = k_drain<W, V, EX>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, W * 2048);
-  cudaMemset(cyc, 0, 148 * 8);
-  k<<<ctas, W * 32, W * 2048>>>(out, s1, cyc, 20);
+  cudaMemset(cyc, 0, 296 * 8);
+  k<<<ctas, (W + EX) * 32, W * 2048>>>(out, s1, cyc, 20, ldy);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("W=%d V=%d error %s\n", W, V, cudaGetErrorString(e));
     return;
   }
-  unsigned long long h[148];
+  unsigned long long h[296];
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
-  double m = 0, mx = 0;
+  double m = 0, mx = 0, m0 = 0;
   for (int i = 0; i < ctas; ++i) {
     m += h[i];
+    m0 += h[148 + i];
     mx = h[i] > mx ? h[i] : mx;
   }
-  printf("W=%2d variant %d, %3d CTAs: %7.0f cycles per 128x512 drain (max %7.0f) = %.2f us at 1.93 GHz\n", W, V,
-         ctas, m / ctas, mx, m / ctas / 1930.0);
+  printf("   first (cold) drain: %7.0f cycles\n", m0 / ctas);
+  printf("W=%2d variant %d, %2d waiting warps, %3d CTAs, row stride %5d: %7.0f cycles per 128x512 drain (max %7.0f) = %.2f us\n",
+         W, V, EX, ctas, ldy, m / ctas, mx, m / ctas / 1930.0);
 }
 
 int main() {
   __half* out;
   float* s1;
   unsigned long long* cyc;
-  cudaMalloc(&out, 148ull * 128 * 512 * 2);
+  cudaMalloc(&out, 148ull * 128 * 28672 * 2);
   cudaMalloc(&s1, 256 * 4);
-  cudaMalloc(&cyc, 148 * 8);
+  cudaMalloc(&cyc, 296 * 8);
   float hs[256];
   for (int i = 0; i < 256; ++i) hs[i] = 0.5f + i * 1e-3f;
   cudaMemcpy(s1, hs, sizeof(hs), cudaMemcpyHostToDevice);
@@ -293,6 +315,9 @@ int main() {
   run<12, 4>(out, s1, cyc);
   run<16, 4>(out, s1, cyc);
   for (int n : {8, 37, 74, 148}) run<12, 0>(out, s1, cyc, n);
+  run<12, 0, 9>(out, s1, cyc, 148, 28672);  // + the kernel's 9 other warps waiting on mbarriers
+  run<12, 0>(out, s1, cyc, 148, 28672);  // OPT-30B fc1 output rows
+  run<12, 0>(out, s1, cyc, 148, 7168);
   run<12, 6>(out, s1, cyc);
   run<16, 6>(out, s1, cyc);
   run<8, 6>(out, s1, cyc);
