@@ -262,10 +262,15 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 // Without kSparse (a layer with more than T channels k != 1, e.g. random-k
 // tests) the masked lanes divide inline instead (ksm bit masks).
 constexpr int kRing = 8;
+// barrier of the T compute threads of k_actquant3 (its producer warp does not take part)
+template <int T>
+__device__ __forceinline__ void compute_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
+}
 // kExact: the launcher guarantees C8 == T * V (every thread owns exactly V
 // chunks), so the per-chunk `c < C8` guards and their branches compile away.
 template <int T, int V, bool kF16, bool kDyn, bool kSparse, bool kExact = false>
-__global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
+__global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
                                                   const float* __restrict__ kv, const float* __restrict__ rkv,
                                                   const uint8_t* __restrict__ ksm, const int* __restrict__ spec,
                                                   int nspec, int K, int Kpad, float act_scale,
@@ -273,6 +278,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
                                                   int depth) {
   extern __shared__ __align__(128) uint8_t sbuf[];
   __shared__ __align__(8) uint64_t full[kRing];
+  __shared__ __align__(8) uint64_t empty[kRing];  // the T compute threads are done with a buffer (one arrive per warp)
   __shared__ float red[2][32];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kEsz = kF16 ? 2 : 4;
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
   const uint32_t bufstride = (rowbytes + 127u) & ~127u;
   const int C8 = K >> 3;
   const int nseg = K / seg;
-  auto issue = [&](int r, int b) {  // thread 0 only
+  auto issue = [&](int r, int b) {  // the producer lane only
     dgqk::mbar_arrive_expect_tx(&full[b], rowbytes);
     for (int sg = 0; sg < nseg; ++sg) {
       const uint8_t* src = static_cast<const uint8_t*>(Xv) +
@@ -294,12 +300,26 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
   // neighbouring kernels, so every thread waits for them before its first access
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
-    for (int b = 0; b < depth; ++b) dgqk::mbar_init(&full[b], 1);
-    dgqk::fence_mbar_init();
     for (int b = 0; b < depth; ++b) {
-      const int r = blockIdx.x + b * gridDim.x;
-      if (r < M) issue(r, b);
+      dgqk::mbar_init(&full[b], 1);
+      dgqk::mbar_init(&empty[b], kW);
     }
+    dgqk::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= T) {
+    // Producer warp: one bulk copy per row into the ring; a row's buffer is
+    // refilled as soon as every compute warp has finished with it.  A TMA
+    // issue holds its lane for ~700 cycles (tools/l2_stream.cu): issued by a
+    // compute thread it delayed that warp's share of every row.
+    if (threadIdx.x == T) {
+      for (int row = blockIdx.x, i = 0; row < M; row += gridDim.x, ++i) {
+        const int bb = i % depth;
+        if (i >= depth) dgqk::mbar_wait(&empty[bb], ((i / depth) - 1) & 1);
+        issue(row, bb);
+      }
+    }
+    return;
   }
   const bool special = kSparse && static_cast<int>(threadIdx.x) < nspec;
   int sj = 0;
@@ -311,9 +331,8 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
   }
   int8_t* pend = nullptr;  // the special's code byte of the previous row
   int pcode = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int b = 0, bprev = -1;
+  int b = 0;
   uint32_t phase = 0;
   for (int row = blockIdx.x, it = 0; row < M; row += gridDim.x, ++it) {
     dgqk::mbar_wait(&full[b], phase);
@@ -332,7 +351,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
         }
         am = fabsf(xs);
       }
-      __syncthreads();  // specials zeroed in the staged row
+      compute_bar<T>();  // specials zeroed in the staged row
     }
     if constexpr (kDyn) {
       uint32_t am16 = 0u;
@@ -382,11 +401,7 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
       for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
       if (lane == 0) red[it & 1][warp] = am;
     }
-    __syncthreads();  // warp maxima published; the previous row's reads and stores retired
-    if (threadIdx.x == 0 && bprev >= 0) {
-      const int nxt = row - static_cast<int>(gridDim.x) + depth * static_cast<int>(gridDim.x);
-      if (nxt < M) issue(nxt, bprev);
-    }
+    compute_bar<T>();  // warp maxima published; the previous row's stores retired
     if (kSparse && pend) *pend = static_cast<int8_t>(pcode);
     float s = act_scale;
     if constexpr (kDyn) {
@@ -430,14 +445,15 @@ __global__ void __launch_bounds__(T) k_actquant3(const void* __restrict__ Xv, si
       pend = qrow + sj;
       pcode = safe ? quant_code_f32(xs, s, inv) : quant_code_f64(xs, s);
     }
-    bprev = b;
+    __syncwarp();
+    if (lane == 0) dgqk::mbar_arrive(&empty[b]);  // this warp's reads of the staged row are done
     if (++b == depth) {
       b = 0;
       phase ^= 1u;
     }
   }
   if constexpr (kSparse) {
-    __syncthreads();
+    compute_bar<T>();
     if (pend) *pend = static_cast<int8_t>(pcode);
   }
 }
@@ -580,9 +596,9 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     auto kern = k_actquant3<T_, (V_ < 0 ? -V_ : V_), F_, D_, S_, (V_ < 0)>;                                    \
     { cudaError_t e_ = dgq_allow_smem(kern, smem); if (e_ != cudaSuccess) return e_; }                        \
     int occ = 1;                                                                                                \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_, smem);                                        \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_ + 32, smem);                                   \
     const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \
-    return launch_pdl(kern, grid, T_, smem, st, X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K, Kpad,      \
+    return launch_pdl(kern, grid, T_ + 32, smem, st, X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K, Kpad, \
                       act_scale, Q, ldq, rs, M, depth);                                                         \
   }
 #define DGQ_AQ3_S(T_, V_, F_, D_)                                                                               \
