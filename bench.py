@@ -591,17 +591,19 @@ def measure_int8_peak(device):
         return None
 
 
-def measure_tcgen05_i8_peak():
+def measure_tcgen05_i8_peak(sustained=False):
     """Dense INT8 tensor peak measured by this library's microbenchmark
     (dgq_measure_i8_peak: every SM pair issuing tcgen05.mma.cta_group::2.kind::i8
-    256x256x32 back to back from shared memory; best of 10 launches)."""
+    256x256x32 back to back from shared memory): best of 10 launches (burst), or
+    ~2500 launches back to back (~3 s) timed as one span (sustained: the clock
+    the GPU holds under continuous tensor load)."""
     import ctypes
 
     import paper_2310_04836_b200 as dgq
 
     t, ms = ctypes.c_double(), ctypes.c_double()
     try:
-        dgq._lib.check(dgq.lib().dgq_measure_i8_peak(10, ctypes.byref(t), ctypes.byref(ms)))
+        dgq._lib.check(dgq.lib().dgq_measure_i8_peak(-2500 if sustained else 10, ctypes.byref(t), ctypes.byref(ms)))
         return t.value
     except Exception:  # noqa: BLE001
         return None
@@ -837,8 +839,12 @@ def run_ours(args):
     hbm_peak, bf16_peak, peak_src = load_peaks()
     i8_proxy = 2.0 * bf16_peak  # dense INT8 = 2x dense BF16 (FP8-class rate); spec 4500
     i8_cublas = measure_int8_peak(device)  # cuBLASLt int8 burst on this GPU
-    i8_tc = measure_tcgen05_i8_peak()  # tcgen05 kind::i8 microbenchmark (the measured tensor-pipe peak)
-    i8_peak = i8_tc or max(i8_proxy, i8_cublas or 0.0)
+    i8_tc = measure_tcgen05_i8_peak()  # tcgen05 kind::i8 microbenchmark, burst (best of 10)
+    # the K5 launches are timed inside a long step: the roofline denominator is
+    # the SUSTAINED rate (~3 s back to back: the clock the GPU holds under
+    # continuous tensor load), the burst figure is reported beside it
+    i8_tc_sus = measure_tcgen05_i8_peak(sustained=True)
+    i8_peak = i8_tc_sus or i8_tc or max(i8_proxy, i8_cublas or 0.0)
     layer = OptLayer(rank, world, device, group, SEQ)
     torch.manual_seed(1234 + 0)
     # the reference's synthetic activations: N(0, 1) with three
@@ -967,7 +973,8 @@ def run_ours(args):
                     detail["configs"] = config_sweeps(device, hbm_peak, i8_peak)
                 except Exception as e:  # noqa: BLE001
                     detail["configs"] = {"error": f"{type(e).__name__}: {e}"}
-            detail["peaks"] = {"hbm_GBps": hbm_peak, "i8_tcgen05_TOPS": i8_tc, "i8_cublaslt_TOPS": i8_cublas,
+            detail["peaks"] = {"hbm_GBps": hbm_peak, "i8_tcgen05_TOPS": i8_tc, "i8_tcgen05_sustained_TOPS": i8_tc_sus,
+                               "i8_cublaslt_TOPS": i8_cublas,
                                "i8_2x_bf16_TOPS": i8_proxy}
         except Exception as e:  # noqa: BLE001  (a detail probe must never sink the headline line)
             detail["error"] = f"{type(e).__name__}: {e}"
@@ -1001,7 +1008,10 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "kernel": "K5 fused DGQ linear (all four launches per step: qkv, out, fc1, fc2)",
                          "achieved": k5_tops, "peak": i8_peak, "unit": "TFLOP/s", "frac": k5_tops / i8_peak,
                          "peak_note": (f"measured here: tcgen05.mma.cta_group::2.kind::i8 microbenchmark "
-                                       f"(dgq_measure_i8_peak, burst, best of 10) = {(i8_tc or 0.0):.0f} TOPS; "
+                                       f"(dgq_measure_i8_peak) sustained over ~3 s back to back = "
+                                       f"{(i8_tc_sus or 0.0):.0f} TOPS (the K5 launches run inside a long step); "
+                                       f"burst (best of 10) {(i8_tc or 0.0):.0f} TOPS (frac "
+                                       f"{k5_tops / (i8_tc or 1e30):.3f}); "
                                        f"also cuBLASLt int8 burst {(i8_cublas or 0.0):.0f} TOPS (frac "
                                        f"{k5_tops / (i8_cublas or 1e30):.3f}), 2 x bf16 {i8_proxy:.0f} "
                                        f"({peak_src}), NVIDIA spec dense INT8 4500 (frac {k5_tops / 4500:.3f})"),

@@ -238,7 +238,10 @@ dgq_status dgq_linear_allgather(const dgq_layer* layer, const int8_t* dXq, size_
 /* ---- measured dense INT8 tensor peak ----------------------------------------
  * The INT8 roofline denominator: every SM pair issues
  * tcgen05.mma.cta_group::2.kind::i8 (256 x 256 x 32, K5p's shape) back to back
- * from shared-memory operands; best of `reps` launches (CUDA events), TOPS out.
+ * from shared-memory operands; best of `reps` launches (CUDA events), TOPS out
+ * (the burst rate).  reps < 0: -reps launches back to back timed as one span —
+ * the sustained rate at the clock the GPU holds under continuous tensor load
+ * (the denominator for kernels timed inside a long step).  reps = 0: 10.
  * Synchronises; runs on the current device. */
 dgq_status dgq_measure_i8_peak(int reps, double* tops, double* best_ms);
 

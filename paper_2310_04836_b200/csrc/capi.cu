@@ -1394,8 +1394,21 @@ dgq_status dgq_measure_i8_peak(int reps, double* tops, double* best_ms) {
   DGQ_CUDA(cudaEventCreate(&e0));
   DGQ_CUDA(cudaEventCreate(&e1));
   float best = 1e30f;
+  if (reps == 0) reps = 10;
   cudaError_t e = dgq_launch_i8_peak(pairs, blocks, sink, st);  // warm-up
-  for (int i = 0; e == cudaSuccess && i < (reps > 0 ? reps : 10); ++i) {
+  if (reps < 0) {
+    // sustained: -reps launches back to back, timed as one span (the clock
+    // the tensor pipe holds under continuous load, e.g. inside a long step)
+    cudaEventRecord(e0, st);
+    for (int i = 0; e == cudaSuccess && i < -reps; ++i) e = dgq_launch_i8_peak(pairs, blocks, sink, st);
+    cudaEventRecord(e1, st);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float ms = 0.0f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    best = ms / static_cast<float>(-reps);
+    reps = 0;
+  }
+  for (int i = 0; e == cudaSuccess && i < reps; ++i) {
     cudaEventRecord(e0, st);
     e = dgq_launch_i8_peak(pairs, blocks, sink, st);
     cudaEventRecord(e1, st);

@@ -803,3 +803,20 @@ def test_linear_allgather_c_abi_world1(cuda, port):
     assert y.shape == (1, 40, 384)
     assert np.array_equal(bits(y[0].cpu().numpy()), bits(out))
     comm.close()
+
+
+def test_measured_i8_peak_burst_and_sustained(cuda):
+    # the roofline denominator (dgq_measure_i8_peak): every SM pair issuing
+    # tcgen05.mma.cta_group::2.kind::i8 back to back; burst (best of launches)
+    # and sustained (launches back to back as one span) are both in the B200's
+    # dense INT8 range and the sustained rate does not exceed the burst one
+    import ctypes
+
+    lib = dgq.lib()
+    t, ms = ctypes.c_double(), ctypes.c_double()
+    dgq._lib.check(lib.dgq_measure_i8_peak(5, ctypes.byref(t), ctypes.byref(ms)))
+    burst = t.value
+    dgq._lib.check(lib.dgq_measure_i8_peak(-50, ctypes.byref(t), ctypes.byref(ms)))
+    sustained = t.value
+    assert 2500 < burst < 5000 and ms.value > 0
+    assert 2500 < sustained <= burst * 1.02
