@@ -78,7 +78,11 @@ __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__
     for (int sub = 0; sub < 2; ++sub) {
       const uint32_t tb = tl + sub * 256;
       const float* sv1 = s_s1 + sub * 256;
-      __half* orow = out + (static_cast<size_t>(blockIdx.x) * 128 + q * 32) * ldy + sub * 256;
+      // rep-dependent column window when the rows are long: 20 reps touch 20x
+      // the lines (more than L2 holds at row stride 28672), as a kernel streaming
+      // a 117 MB output does
+      const size_t cw = ldy >= 28672 ? static_cast<size_t>(rep % 28) * 1024 : 0;
+      __half* orow = out + (static_cast<size_t>(blockIdx.x) * 128 + q * 32) * ldy + sub * 256 + cw;
       uint32_t r[2][16];
       if (V == 3) tmem_ld16(tb + cbeg, r[0]);
 #pragma unroll 1
