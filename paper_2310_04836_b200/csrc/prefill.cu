@@ -1154,7 +1154,7 @@ static bool sk_balance() {
 // Stream-K split balanced for the per-segment cost.  A pair's time is its MMA
 // units plus a fixed cost per segment (tile piece) it touches: the exposed
 // epilogue (S = 2: one accumulator set), a contributor's parked partial or an
-// owner's fix-up, ~9 us = ~15 k-block steps of a 512-token tile.  An even
+// owner's fix-up (E = 8 k-block steps of a 512-token tile measured best).  An even
 // split of the units gives the pairs that touch one more tile one more such
 // stop; here the smallest per-pair cost C for which a greedy walk (each pair
 // takes units while units + E x segments <= C) covers everything with at most
@@ -1237,7 +1237,12 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
   p.sk_b[0] = -1;
   if (p.stream_k && sk_balance()) {
     const long long U = static_cast<long long>((p.M + 256 * S - 1) / (256 * S)) * p.n_pair_tiles * p.k_blocks;
-    const int used = sk_bounds(U, p.k_blocks, ncl, S == 2 ? 15 : 5, p.sk_b);
+    static const int e_env = [] {  // tools: DGQ_PF_E overrides the per-segment cost (k-block steps)
+      const char* e = getenv("DGQ_PF_E");
+      return e ? atoi(e) : -1;
+    }();
+    const int E = e_env >= 0 ? e_env : (S == 2 ? 8 : 5);  // tools/ A/B at 2048 tokens: E = 0 / 8 / 15 / 25 -> 934 / 920 / 925 / 930 us
+    const int used = sk_bounds(U, p.k_blocks, ncl, E, p.sk_b);
     if (used > 0) ncl = used; else p.sk_b[0] = -1;
   }
   cfg.gridDim = dim3(2 * ncl);
