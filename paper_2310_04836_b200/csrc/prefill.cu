@@ -1241,7 +1241,7 @@ static cudaError_t launch_pf(const CUtensorMap& tmA, const CUtensorMap& tmY, con
       const char* e = getenv("DGQ_PF_E");
       return e ? atoi(e) : -1;
     }();
-    const int E = e_env >= 0 ? e_env : (S == 2 ? 8 : 5);  // tools/ A/B at 2048 tokens: E = 0 / 8 / 15 / 25 -> 934 / 920 / 925 / 930 us
+    const int E = e_env >= 0 ? e_env : (S == 2 ? 8 : 5);  // A/B at 2048 tokens: E = 0 / 8 / 15 / 25 -> 934 / 920 / 925 / 930 us
     const int used = sk_bounds(U, p.k_blocks, ncl, E, p.sk_b);
     if (used > 0) ncl = used; else p.sk_b[0] = -1;
   }
