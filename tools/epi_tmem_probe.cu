@@ -257,6 +257,22 @@ __global__ void __launch_bounds__(W * 32, 1) k_drain128(__half* __restrict__ out
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// L2 read stream (the main loops of the other pairs): each CTA streams a
+// 24 MB buffer (L2-resident) with 16-byte loads until `stop` is set
+__global__ void k_l2_stream(const uint4* __restrict__ src, size_t n, volatile int* stop, unsigned long long* sink) {
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  size_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  int iter = 0;
+  while (true) {
+    const uint4 v = src[i];
+    acc.x ^= v.x; acc.y += v.y;
+    i += static_cast<size_t>(gridDim.x) * blockDim.x;
+    if (i >= n) i -= n;
+    if ((++iter & 255) == 0 && *stop) break;
+  }
+  if (acc.x == 0x12345678u) *sink = acc.y;
+}
+
 template <int W>
 static void run128(__half* out, const float* s1, unsigned long long* cyc) {
   auto k = k_drain128<W>;
@@ -325,6 +341,39 @@ int main() {
   run<12, 6>(out, s1, cyc);
   run<16, 6>(out, s1, cyc);
   run<8, 6>(out, s1, cyc);
+  {
+    // the drain on 74 SMs while 74 other SMs stream L2 reads
+    uint4* src;
+    int* stop;
+    unsigned long long* sink;
+    const size_t n = (24u << 20) / 16;
+    cudaMalloc(&src, n * 16);
+    cudaMemset(src, 1, n * 16);
+    cudaMalloc(&stop, 4);
+    cudaMalloc(&sink, 8);
+    cudaMemset(stop, 0, 4);
+    cudaStream_t sa, sb;
+    cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking);
+    k_l2_stream<<<74, 1024, 0, sb>>>(src, n, stop, sink);
+    auto k = k_drain<12, 0, 0>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 2048);
+    cudaMemset(cyc, 0, 296 * 8);
+    k<<<74, 12 * 32, 12 * 2048, sa>>>(out, s1, cyc, 20, 28672);
+    cudaStreamSynchronize(sa);
+    int one = 1;
+    cudaMemcpy(stop, &one, 4, cudaMemcpyHostToDevice);
+    cudaDeviceSynchronize();
+    unsigned long long h[148];
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    double m = 0;
+    int cnt = 0;
+    for (int i = 0; i < 148; ++i)
+      if (h[i]) { m += h[i]; ++cnt; }
+    printf("W=12 drain on %d CTAs beside an L2 read stream on 74 SMs: %7.0f cycles = %.2f us\n", cnt, m / cnt,
+           m / cnt / 1930.0);
+  }
+  run<12, 0>(out, s1, cyc, 74, 28672);
   run128<8>(out, s1, cyc);
   run128<16>(out, s1, cyc);
   return 0;
