@@ -7,7 +7,8 @@
 // sub-tiles), averaged over CTAs, for W = 8 / 12 / 16 and variants:
 //   0 = epi_direct's structure, 1 = TMEM loads only, 2 = 32-column loads,
 //   3 = the next unit's first load issued before the stores (no register cap here),
-//   4 = no global stores, 6 = 256-bit global stores; and the W = 12 drain on
+//   4 = no global stores, 6 = 256-bit global stores, 7 = no staging: each lane
+//   stores its row's 16 values with one 32-byte store; and the W = 12 drain on
 //   8 / 37 / 74 / 148 CTAs, and 128-byte staging rows
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2310_04836_b200/csrc -o tools/_bin/epi_tmem_probe tools/epi_tmem_probe.cu
 #include <cuda_fp16.h>
@@ -115,6 +116,22 @@ __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__
           } else if (V == 3 && c0 + 32 < cend) {
             tmem_ld16(tb + c0 + 32, r[0]);
           }
+          if (V == 7) {  // 16 values of this lane's row -> one 32-byte store, no staging
+            uint32_t h[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float a = __fmul_rn(__fmul_rn(__int2float_rn(static_cast<int32_t>(cur[2 * k])), rsm), sv1[c0 + c16 + 2 * k]);
+              const float b2 = __fmul_rn(__fmul_rn(__int2float_rn(static_cast<int32_t>(cur[2 * k + 1])), rsm),
+                                         sv1[c0 + c16 + 2 * k + 1]);
+              const __half2 hh = __floats2half2_rn(a, b2);
+              h[k] = *reinterpret_cast<const uint32_t*>(&hh);
+            }
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(orow + lane * ldy + c0 + c16),
+                         "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7])
+                         : "memory");
+            if (c16 == 0) tmem_ld_wait();
+            continue;
+          }
 #pragma unroll
           for (int c8 = 0; c8 < 16; c8 += 8) {
             const int c1 = c16 + c8;
@@ -134,6 +151,7 @@ __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__
           }
           if (V != 2 && c16 == 0) tmem_ld_wait();
         }
+        if (V == 7) continue;
         __syncwarp();
         const int ch = lane & 3;
         if (V == 4) {
@@ -338,6 +356,10 @@ int main() {
   run<12, 0, 9>(out, s1, cyc, 148, 28672);  // + the kernel's 9 other warps waiting on mbarriers
   run<12, 0>(out, s1, cyc, 148, 28672);  // OPT-30B fc1 output rows
   run<12, 0>(out, s1, cyc, 148, 7168);
+  run<12, 7>(out, s1, cyc);
+  run<12, 7>(out, s1, cyc, 148, 28672);
+  run<16, 7>(out, s1, cyc);
+  run<8, 7>(out, s1, cyc);
   run<12, 6>(out, s1, cyc);
   run<16, 6>(out, s1, cyc);
   run<8, 6>(out, s1, cyc);
