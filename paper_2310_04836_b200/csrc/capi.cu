@@ -883,10 +883,10 @@ static dgq_status run_decode(const DecodeSub* subs, int count, int g, size_t k_p
   {
     // units per stage: as many as the TMEM partial ring allows with >= 2 slots
     const int per = d.gpk * pl.bn;
-    const int ku = 128 / per;
+    const int ku = dgq_decode_partial_cols() / 2 / per;
     const int ups = dgq_decode_units_per_stage(pl.bn);
     d.ku = ku < 1 ? 1 : (ku > ups ? ups : ku);
-    const int room = 256 / (d.ku * per);  // TMEM columns [256, 512) hold the partial ring
+    const int room = dgq_decode_partial_cols() / (d.ku * per);  // TMEM columns of the partial ring
     d.sd_log2 = room >= 8 ? 3 : (room >= 4 ? 2 : (room >= 2 ? 1 : 0));
   }
   CUtensorMap tmB;

@@ -50,10 +50,13 @@
 namespace dgqk {
 
 namespace dec {
-// TMEM (512 columns): A ring [kSA][UPS x 32] in [0, 256), partial ring
+// TMEM (512 columns): A ring [kSA][UPS x 32] in [0, kDCol0), partial ring
 // [SD][ku x gpk x BN] in [256, 512).
-constexpr int kSA = 2;
-constexpr int kDCol0 = 256;
+#ifndef DGQ_DEC_SA
+#define DGQ_DEC_SA 2  // TMEM A slots (stages of UPS units x 32 columns); tools A/B
+#endif
+constexpr int kSA = DGQ_DEC_SA;
+constexpr int kDCol0 = kSA * 128;  // A ring [0, kSA x 128), partial ring [kDCol0, 512)
 constexpr int kMaxSD = 8;
 constexpr int kMmaWarps = 2;     // warps 1..2: MMA issuers (warp 1 also owns TMEM)
 constexpr int kUnpackWarps = 8;  // warps 4..11; epilogue warps 12..15
@@ -506,6 +509,8 @@ static cudaError_t launch_dec(const CUtensorMap& tmB, const DgqDecodeParams& p, 
 }  // namespace dgqk
 
 using namespace dgqk;
+
+int dgq_decode_partial_cols() { return 512 - dec::kDCol0; }
 
 size_t dgq_decode_smem_bytes(int bn, int sl, uint32_t chunk_stride) {
   return 1024 + static_cast<size_t>(sl) * (bn * 128 + chunk_stride) +

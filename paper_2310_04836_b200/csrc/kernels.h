@@ -112,6 +112,7 @@ struct DgqDecodeParams {
   int trace_cta;
   int pre_stages;  // stages whose weights are requested before griddepcontrol.wait (>= 1)
 };
+int dgq_decode_partial_cols();  // TMEM columns K5d keeps for its partial ring
 size_t dgq_decode_smem_bytes(int bn, int sl, uint32_t chunk_stride);
 int dgq_decode_stages(int bn);            // units of shared-memory ring (stages x units per stage)
 int dgq_decode_units_per_stage(int bn);   // box depth of the 3-D Xq tensor map
