@@ -264,13 +264,16 @@ __global__ void __launch_bounds__(T) k_actquant2(const void* __restrict__ Xv, si
 constexpr int kRing = 8;
 // barrier of the T compute threads of k_actquant3 (its producer warp does not take part)
 template <int T>
-__device__ __forceinline__ void compute_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
+__device__ __forceinline__ void compute_bar(int grp) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(T) : "memory");
 }
 // kExact: the launcher guarantees C8 == T * V (every thread owns exactly V
 // chunks), so the per-chunk `c < C8` guards and their branches compile away.
-template <int T, int V, bool kF16, bool kDyn, bool kSparse, bool kExact = false>
-__global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
+// G > 1: G independent groups of T compute threads per CTA, each taking every
+// G-th row of the CTA, each with its own named barrier — one group's barrier
+// waits overlap the other's passes.
+template <int T, int V, bool kF16, bool kDyn, bool kSparse, bool kExact = false, int G = 1>
+__global__ void __launch_bounds__(G * T + 32, G * T >= 512 ? 1 : 2) k_actquant3(const void* __restrict__ Xv, size_t ldx, int seg, size_t seg_stride,
                                                   const float* __restrict__ kv, const float* __restrict__ rkv,
                                                   const uint8_t* __restrict__ ksm, const int* __restrict__ spec,
                                                   int nspec, int K, int Kpad, float act_scale,
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
   extern __shared__ __align__(128) uint8_t sbuf[];
   __shared__ __align__(8) uint64_t full[kRing];
   __shared__ __align__(8) uint64_t empty[kRing];  // the T compute threads are done with a buffer (one arrive per warp)
-  __shared__ float red[2][32];
+  __shared__ float red_all[G][2][32];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kEsz = kF16 ? 2 : 4;
   constexpr int kW = T / 32;
@@ -307,12 +310,12 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
     dgqk::fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x >= T) {
+  if (threadIdx.x >= G * T) {
     // Producer warp: one bulk copy per row into the ring; a row's buffer is
     // refilled as soon as every compute warp has finished with it.  A TMA
     // issue holds its lane for ~700 cycles (tools/l2_stream.cu): issued by a
     // compute thread it delayed that warp's share of every row.
-    if (threadIdx.x == T) {
+    if (threadIdx.x == G * T) {
       for (int row = blockIdx.x, i = 0; row < M; row += gridDim.x, ++i) {
         const int bb = i % depth;
         if (i >= depth) dgqk::mbar_wait(&empty[bb], ((i / depth) - 1) & 1);
@@ -321,20 +324,24 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
     }
     return;
   }
-  const bool special = kSparse && static_cast<int>(threadIdx.x) < nspec;
+  const int grp = static_cast<int>(threadIdx.x) / T;  // this thread's row group
+  const int tid = static_cast<int>(threadIdx.x) % T;  // index inside the group
+  float(&red)[2][32] = red_all[grp];
+  const bool special = kSparse && tid < nspec;
   int sj = 0;
   float sk = 1.0f, srk = 1.0f;
   if (special) {
-    sj = __ldg(spec + threadIdx.x);
+    sj = __ldg(spec + tid);
     sk = __ldg(kv + sj);
     srk = __ldg(rkv + sj);
   }
   int8_t* pend = nullptr;  // the special's code byte of the previous row
   int pcode = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int b = 0;
-  uint32_t phase = 0;
-  for (int row = blockIdx.x, it = 0; row < M; row += gridDim.x, ++it) {
+  const int lane = threadIdx.x & 31, warp = tid >> 5;
+  for (int row = blockIdx.x + grp * static_cast<int>(gridDim.x), it = 0, i = grp; row < M;
+       row += G * static_cast<int>(gridDim.x), ++it, i += G) {
+    const int b = i % depth;  // row i of this CTA sits in buffer i % depth
+    const uint32_t phase = (i / depth) & 1;
     dgqk::mbar_wait(&full[b], phase);
     uint8_t* buf = sbuf + b * bufstride;
     float am = 0.0f, xs = 0.0f;
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
         }
         am = fabsf(xs);
       }
-      compute_bar<T>();  // specials zeroed in the staged row
+      compute_bar<T>(grp);  // specials zeroed in the staged row
     }
     if constexpr (kDyn) {
       uint32_t am16 = 0u;
@@ -359,13 +366,13 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
       if constexpr (kF16 && kSparse) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const int c = threadIdx.x + v * T;
+          const int c = tid + v * T;
           r16[v] = (kExact || c < C8) ? *reinterpret_cast<const uint4*>(buf + c * 16) : make_uint4(0u, 0u, 0u, 0u);
         }
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const int c = threadIdx.x + v * T;
+        const int c = tid + v * T;
         if (kExact || c < C8) {
           if constexpr (kF16) {
             const uint4 raw = kSparse ? r16[kSparse ? v : 0] : *reinterpret_cast<const uint4*>(buf + c * 16);
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
       for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
       if (lane == 0) red[it & 1][warp] = am;
     }
-    compute_bar<T>();  // warp maxima published; the previous row's stores retired
+    compute_bar<T>(grp);  // warp maxima published; the previous row's stores retired
     if (kSparse && pend) *pend = static_cast<int8_t>(pcode);
     float s = act_scale;
     if constexpr (kDyn) {
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
       for (int o = 16; o > 0; o >>= 1) w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
       s = dynamic_row_scale(w);
     }
-    if (threadIdx.x == 0) rs[row] = s;
+    if (tid == 0) rs[row] = s;
     int8_t* qrow = Q + static_cast<size_t>(row) * ldq;
     uint2* qr = reinterpret_cast<uint2*>(qrow);
     const bool safe = scale_is_safe(s);
@@ -423,7 +430,7 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
       uint4 raw[kG][kF16 ? 1 : 2];
 #pragma unroll
       for (int v = v0; v < v0 + kG && v < V; ++v) {
-        const int c = threadIdx.x + v * T;
+        const int c = tid + v * T;
         if (kExact || c < C8) {
           raw[v - v0][0] = *reinterpret_cast<const uint4*>(buf + c * 8 * kEsz);
           if constexpr (!kF16) raw[v - v0][1] = *reinterpret_cast<const uint4*>(buf + c * 32 + 16);
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
       }
 #pragma unroll
       for (int v = v0; v < v0 + kG && v < V; ++v) {
-        const int c = threadIdx.x + v * T;
+        const int c = tid + v * T;
         if (kExact || c < C8) {
           float x[8];
           unpack8<kF16>(raw[v - v0], x);
@@ -440,20 +447,16 @@ __global__ void __launch_bounds__(T + 32, T >= 512 ? 1 : 2) k_actquant3(const vo
         }
       }
     }
-    for (int c = C8 + threadIdx.x; c < (Kpad >> 3); c += T) qr[c] = make_uint2(0u, 0u);
+    for (int c = C8 + tid; c < (Kpad >> 3); c += T) qr[c] = make_uint2(0u, 0u);
     if (special) {
       pend = qrow + sj;
       pcode = safe ? quant_code_f32(xs, s, inv) : quant_code_f64(xs, s);
     }
     __syncwarp();
     if (lane == 0) dgqk::mbar_arrive(&empty[b]);  // this warp's reads of the staged row are done
-    if (++b == depth) {
-      b = 0;
-      phase ^= 1u;
-    }
   }
   if constexpr (kSparse) {
-    compute_bar<T>();
+    compute_bar<T>(grp);
     if (pend) *pend = static_cast<int8_t>(pcode);
   }
 }
@@ -539,6 +542,17 @@ static int aq_decode_clusters() {
   }();
   return v;
 }
+// row groups per persistent K1 CTA on the fc2-shaped input: two groups of 256
+// threads, each on every other row with its own barrier, overlap one group's
+// barrier waits with the other's passes (tools/k1_ab.py, 2048 x 28672 FP16:
+// 42.4 -> 36.0 us, 0.75 of HBM).  DGQ_K1_G=1: one group of 512 (A/B)
+static int aq_groups() {
+  static const int v = [] {
+    const char* e = getenv("DGQ_K1_G");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
 static int aq_threads() {
   static const int v = [] {
     const char* e = getenv("DGQ_K1_T");
@@ -591,44 +605,45 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     if (!depth) depth = 3;
     while (depth > 3 && depth * bufstride > 220 * 1024) --depth;
     const size_t smem = depth * bufstride;
-#define DGQ_AQ3_K(T_, V_, F_, D_, S_)                                                                          \
+#define DGQ_AQ3_K(T_, V_, F_, D_, S_, G_)                                                                      \
   {                                                                                                             \
-    auto kern = k_actquant3<T_, (V_ < 0 ? -V_ : V_), F_, D_, S_, (V_ < 0)>;                                    \
+    auto kern = k_actquant3<T_, (V_ < 0 ? -V_ : V_), F_, D_, S_, (V_ < 0), G_>;                                \
     { cudaError_t e_ = dgq_allow_smem(kern, smem); if (e_ != cudaSuccess) return e_; }                        \
     int occ = 1;                                                                                                \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T_ + 32, smem);                                   \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G_ * T_ + 32, smem);                              \
     const int grid = std::min(M, n_sm * std::max(occ, 1));                                                      \
-    return launch_pdl(kern, grid, T_ + 32, smem, st, X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K, Kpad, \
-                      act_scale, Q, ldq, rs, M, depth);                                                         \
+    return launch_pdl(kern, grid, G_ * T_ + 32, smem, st, X, ldx, seg, seg_stride, k, rk, ksm, spec, nspec, K,  \
+                      Kpad, act_scale, Q, ldq, rs, M, depth);                                                   \
   }
-#define DGQ_AQ3_S(T_, V_, F_, D_)                                                                               \
+#define DGQ_AQ3_S(T_, V_, F_, D_, G_)                                                                           \
   {                                                                                                             \
-    if (ksm && nspec <= T_) DGQ_AQ3_K(T_, V_, F_, D_, true)                                                     \
-    DGQ_AQ3_K(T_, V_, F_, D_, false)                                                                            \
+    if (ksm && nspec <= T_) DGQ_AQ3_K(T_, V_, F_, D_, true, G_)                                                 \
+    DGQ_AQ3_K(T_, V_, F_, D_, false, G_)                                                                        \
   }
-#define DGQ_AQ3(T_, V_)                                                                                         \
+#define DGQ_AQ3(T_, V_, G_)                                                                                     \
   {                                                                                                             \
     if (f16) {                                                                                                  \
-      if (dynamic) DGQ_AQ3_S(T_, V_, true, true)                                                                \
-      DGQ_AQ3_S(T_, V_, true, false)                                                                            \
+      if (dynamic) DGQ_AQ3_S(T_, V_, true, true, G_)                                                            \
+      DGQ_AQ3_S(T_, V_, true, false, G_)                                                                        \
     }                                                                                                           \
-    if (dynamic) DGQ_AQ3_S(T_, V_, false, true)                                                                 \
-    DGQ_AQ3_S(T_, V_, false, false)                                                                             \
+    if (dynamic) DGQ_AQ3_S(T_, V_, false, true, G_)                                                             \
+    DGQ_AQ3_S(T_, V_, false, false, G_)                                                                         \
   }
 #define DGQ_AQ3_V(T_)                                                                                           \
   {                                                                                                             \
-    if (need <= 4) DGQ_AQ3(T_, 4)                                                                               \
-    if (need <= 8) DGQ_AQ3(T_, 8)                                                                               \
-    if (need <= 12) DGQ_AQ3(T_, 12)                                                                             \
-    DGQ_AQ3(T_, 16)                                                                                             \
+    if (need <= 4) DGQ_AQ3(T_, 4, 1)                                                                            \
+    if (need <= 8) DGQ_AQ3(T_, 8, 1)                                                                            \
+    if (need <= 12) DGQ_AQ3(T_, 12, 1)                                                                          \
+    DGQ_AQ3(T_, 16, 1)                                                                                          \
   }
     // exact shapes (C8 == T * V): no per-chunk guards, no idle chunk slots
     // (tools/k1_ab.py, 2048 rows, smoothed k: K = 28672 f16 50.7 -> 43.8 us at
     // T = 512; K = 7168 f16 16.3 -> 14.4 us, f32 20.2 -> 19.6 us at T = 128)
-    if (T == 128 && C8 == 7 * 128) DGQ_AQ3(128, -7)
-    if (T == 128 && C8 == 4 * 128) DGQ_AQ3(128, -4)
-    if (T == 256 && C8 == 4 * 256) DGQ_AQ3(256, -4)
-    if (T == 512 && C8 == 7 * 512) DGQ_AQ3(512, -7)
+    if (T == 128 && C8 == 7 * 128) DGQ_AQ3(128, -7, 1)
+    if (T == 128 && C8 == 4 * 128) DGQ_AQ3(128, -4, 1)
+    if (T == 256 && C8 == 4 * 256) DGQ_AQ3(256, -4, 1)
+    if (T == 512 && C8 == 7 * 512 && aq_groups() == 2) DGQ_AQ3(256, -14, 2)  // two row groups of 256 threads
+    if (T == 512 && C8 == 7 * 512) DGQ_AQ3(512, -7, 1)
     if (T == 128) DGQ_AQ3_V(128)
     if (T == 256) DGQ_AQ3_V(256)
     DGQ_AQ3_V(512)
