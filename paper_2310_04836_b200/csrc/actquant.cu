@@ -542,10 +542,11 @@ static int aq_decode_clusters() {
   }();
   return v;
 }
-// row groups per persistent K1 CTA on the fc2-shaped input: two groups of 256
-// threads, each on every other row with its own barrier, overlap one group's
-// barrier waits with the other's passes (tools/k1_ab.py, 2048 x 28672 FP16:
-// 42.4 -> 36.0 us, 0.75 of HBM).  DGQ_K1_G=1: one group of 512 (A/B)
+// row groups per persistent K1 CTA on the exact shapes: two groups, each on
+// every other row with its own barrier, overlap one group's barrier waits with
+// the other's passes (tools/k1_ab.py, 2048 rows: 28672 FP16 42.4 -> 36.0 us,
+// 7168 FP32 18.4 -> 15.2 us, 7168 FP16 13.0 -> 12.5 us).  DGQ_K1_G=1: one
+// group (A/B)
 static int aq_groups() {
   static const int v = [] {
     const char* e = getenv("DGQ_K1_G");
@@ -639,11 +640,12 @@ cudaError_t dgq_launch_actquant2(const void* X, bool f16, size_t ldx, int seg, s
     // exact shapes (C8 == T * V): no per-chunk guards, no idle chunk slots
     // (tools/k1_ab.py, 2048 rows, smoothed k: K = 28672 f16 50.7 -> 43.8 us at
     // T = 512; K = 7168 f16 16.3 -> 14.4 us, f32 20.2 -> 19.6 us at T = 128)
-    if (T == 128 && C8 == 7 * 128) DGQ_AQ3(128, -7, 1)
-    if (T == 128 && C8 == 4 * 128) DGQ_AQ3(128, -4, 1)
-    if (T == 256 && C8 == 4 * 256) DGQ_AQ3(256, -4, 1)
-    if (T == 512 && C8 == 7 * 512 && aq_groups() == 2) DGQ_AQ3(256, -14, 2)  // two row groups of 256 threads
-    if (T == 512 && C8 == 7 * 512) DGQ_AQ3(512, -7, 1)
+    // and two independent row groups per CTA (aq_groups)
+    const bool g2 = aq_groups() == 2;
+    if (T == 128 && C8 == 7 * 128) { if (g2) DGQ_AQ3(128, -7, 2) DGQ_AQ3(128, -7, 1) }
+    if (T == 128 && C8 == 4 * 128) { if (g2) DGQ_AQ3(128, -4, 2) DGQ_AQ3(128, -4, 1) }
+    if (T == 256 && C8 == 4 * 256) { if (g2) DGQ_AQ3(256, -4, 2) DGQ_AQ3(256, -4, 1) }
+    if (T == 512 && C8 == 7 * 512) { if (g2) DGQ_AQ3(256, -14, 2) DGQ_AQ3(512, -7, 1) }
     if (T == 128) DGQ_AQ3_V(128)
     if (T == 256) DGQ_AQ3_V(256)
     DGQ_AQ3_V(512)
