@@ -8,7 +8,7 @@
 //   0 = epi_direct's structure, 1 = TMEM loads only, 2 = 32-column loads,
 //   3 = the next unit's first load issued before the stores (no register cap here),
 //   4 = no global stores, 6 = 256-bit global stores, 7 = no staging: each lane
-//   stores its row's 16 values with one 32-byte store; and the W = 12 drain on
+//   stores its row's 16 values with one 32-byte store, 8 / 9 = .cs / .cg stores; and the W = 12 drain on
 //   8 / 37 / 74 / 148 CTAs, and 128-byte staging rows
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2310_04836_b200/csrc -o tools/_bin/epi_tmem_probe tools/epi_tmem_probe.cu
 #include <cuda_fp16.h>
@@ -177,7 +177,12 @@ __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__
         for (int it = 0; it < 4; ++it) {
           const int row = it * 8 + (lane >> 2);
           const uint4 v = *reinterpret_cast<const uint4*>(stg + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4));
-          *reinterpret_cast<uint4*>(orow + row * ldy + c0 + ch * 8) = v;
+          if (V == 8)  // streaming store (.cs: evict-first)
+            __stcs(reinterpret_cast<uint4*>(orow + row * ldy + c0 + ch * 8), v);
+          else if (V == 9)  // L2-cached only (.cg)
+            __stcg(reinterpret_cast<uint4*>(orow + row * ldy + c0 + ch * 8), v);
+          else
+            *reinterpret_cast<uint4*>(orow + row * ldy + c0 + ch * 8) = v;
         }
         __syncwarp();
       }
@@ -356,6 +361,9 @@ int main() {
   run<12, 0, 9>(out, s1, cyc, 148, 28672);  // + the kernel's 9 other warps waiting on mbarriers
   run<12, 0>(out, s1, cyc, 148, 28672);  // OPT-30B fc1 output rows
   run<12, 0>(out, s1, cyc, 148, 7168);
+  run<12, 8>(out, s1, cyc, 148, 28672);
+  run<12, 9>(out, s1, cyc, 148, 28672);
+  run<12, 0>(out, s1, cyc, 148, 28672);
   run<12, 7>(out, s1, cyc);
   run<12, 7>(out, s1, cyc, 148, 28672);
   run<16, 7>(out, s1, cyc);
