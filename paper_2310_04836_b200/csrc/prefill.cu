@@ -460,7 +460,7 @@ __device__ __forceinline__ void epi_direct(const DgqGemmParams& p, const DgqDeco
         const int row = it * kRPP + static_cast<int>(lane / kNC);
         const int rsw = kNC == 8 ? (row & 7) : ((row >> 1) & 3);
         const uint4 v = *reinterpret_cast<const uint4*>(stg + row * kRowB + ((ch ^ rsw) << 4));
-        *reinterpret_cast<uint4*>(out0 + row * row_bytes) = v;
+        __stcg(reinterpret_cast<uint4*>(out0 + row * row_bytes), v);  // L2 only: written once (3 % faster drain in tools/epi_tmem_probe.cu, neutral in the layer)
       }
     } else {
 #pragma unroll 1
