@@ -896,7 +896,7 @@ def run_ours(args):
     # `ncu --set full` launch per shape, tools/profile_r02.sh): average bytes per
     # launch over the step's four K5 launches (the out projection has q's shape)
     traffic, traffic_by = None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r02h.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r02i.json")
     if os.path.exists(prof) and world == 1:
         try:
             pr = json.load(open(prof))
