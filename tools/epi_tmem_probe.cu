@@ -20,6 +20,14 @@
 #include "ptx.cuh"
 using namespace dgqk;
 
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst)) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t t) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(t) : "memory");
+}
+
 template <int W, int V, int EX = 0>
 __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__ out, const float* __restrict__ s1g,
                                                     unsigned long long* cyc, int reps, int ldy_ = 512) {
@@ -36,8 +44,14 @@ __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__
     mbar_init(&stop, W);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (warp == 0) {
+    if (V == 10)
+      tmem_alloc_pair(&tslot);  // as the pair kernel allocates (2-CTA cluster launch)
+    else
+      tmem_alloc<512>(&tslot);
+  }
   tc_fence_before();
+  if (V == 10) asm volatile("barrier.cluster.arrive.aligned; barrier.cluster.wait.aligned;" ::: "memory");
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tslot;
@@ -196,7 +210,12 @@ __global__ void __launch_bounds__((W + EX) * 32, 1) k_drain(__half* __restrict__
   if (threadIdx.x == 0) cyc[blockIdx.x] = total / reps;
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (V == 10) {
+    asm volatile("barrier.cluster.arrive.aligned; barrier.cluster.wait.aligned;" ::: "memory");
+    if (warp == 0) tmem_dealloc_pair(tmem);
+  } else if (warp == 0) {
+    tmem_dealloc<512>(tmem);
+  }
 }
 
 // 128-byte staging rows (64-column units, 4 KB per warp): each 16-byte store
@@ -361,6 +380,30 @@ int main() {
   run<12, 0, 9>(out, s1, cyc, 148, 28672);  // + the kernel's 9 other warps waiting on mbarriers
   run<12, 0>(out, s1, cyc, 148, 28672);  // OPT-30B fc1 output rows
   run<12, 0>(out, s1, cyc, 148, 7168);
+  {
+    auto k = k_drain<12, 10, 0>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 2048);
+    cudaMemset(cyc, 0, 296 * 8);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(148);
+    cfg.blockDim = dim3(12 * 32);
+    cfg.dynamicSmemBytes = 12 * 2048;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, out, (const float*)s1, cyc, 20, 28672);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    unsigned long long h[148];
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    double m = 0;
+    for (int i = 0; i < 148; ++i) m += h[i];
+    printf("W=12 drain, TMEM allocated cta_group::2 in 2-CTA clusters: %7.0f cycles = %.2f us (%s)\n", m / 148,
+           m / 148 / 1930.0, cudaGetErrorString(e));
+  }
   run<12, 8>(out, s1, cyc, 148, 28672);
   run<12, 9>(out, s1, cyc, 148, 28672);
   run<12, 0>(out, s1, cyc, 148, 28672);
